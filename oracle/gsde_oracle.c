@@ -68,9 +68,10 @@ static const double INV_2_53 = 1.0 / 9007199254740992.0;
 /* rng.py:69-72 */
 double orc_u64_to_uniform(uint64_t r) { return (double)(r >> 11) * INV_2_53; }
 
-/* rng.py:81-134: AS241 layout, two Newton polishes in the far tail */
-double orc_norm_ppf(double p) {
-  double q = p - 0.5;
+/* rng.py:81-134: AS241 layout, two Newton polishes in the far tail.
+ * Written on (q = p - 1/2, pt = min(p, 1-p)) so the lattice map below can pass
+ * both exactly. */
+static double norm_ppf_qt(double q, double pt) {
   if (fabs(q) <= 0.425) {
     double r = 0.180625 - q * q;
     double num = (((((((2.5090809287301226727e3 * r + 3.3430575583588128105e4) * r +
@@ -83,8 +84,7 @@ double orc_norm_ppf(double p) {
                    4.2313330701600911252e1) * r + 1.0);
     return q * num / den;
   }
-  double r = q < 0.0 ? p : 1.0 - p;
-  r = sqrt(-log(r));
+  double r = sqrt(-log(pt));
   if (r <= 5.0) {
     double rr = r - 1.6;
     double num = (((((((7.74545014278341407640e-4 * rr + 2.27238449892691845833e-2) * rr +
@@ -108,7 +108,6 @@ double orc_norm_ppf(double p) {
                    1.48753612908506148525e-2) * rr + 1.36929880922735805310e-1) * rr +
                  5.99832206555887937690e-1) * rr + 1.0);
   double val = num / den;
-  double pt = q < 0.0 ? p : 1.0 - p;
   double x = -val;
   for (int i = 0; i < 2; ++i) {
     double cdf = 0.5 * erfc(-x / 1.4142135623730951);
@@ -119,9 +118,22 @@ double orc_norm_ppf(double p) {
   return q < 0.0 ? -val : val;
 }
 
-/* rng.py:137-143: centred 53-bit lattice */
+double orc_norm_ppf(double p) {
+  double q = p - 0.5;
+  return norm_ppf_qt(q, q < 0.0 ? p : 1.0 - p);
+}
+
+/* rng.py:137-143: p = (n + 1/2) 2^-53 on the centred 53-bit lattice.  Evaluated
+ * exactly: q = (n - 2^52 + 1/2) 2^-53 and min(p, 1-p) are both representable,
+ * whereas rounding p first (strict IEEE reading of the Python source) maps the
+ * top lattice point to p = 1 and returns NaN.  The reference's compiled
+ * (numba fastmath) code returns the finite quantile there, as does this. */
 double orc_u64_to_normal(uint64_t r) {
-  return orc_norm_ppf(((double)(r >> 11) + 0.5) * INV_2_53);
+  int64_t n = (int64_t)(r >> 11);
+  double q = ((double)(n - 4503599627370496LL) + 0.5) * INV_2_53;
+  double pt = q < 0.0 ? ((double)n + 0.5) * INV_2_53
+                      : ((double)(9007199254740992LL - n) - 0.5) * INV_2_53;
+  return norm_ppf_qt(q, pt);
 }
 
 /* ---- packed graph + field (graph.py:102-125, coefficients.py:121-152) -- */
