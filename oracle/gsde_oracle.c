@@ -419,3 +419,32 @@ int orc_max_threads(void) {
   return 1;
 #endif
 }
+
+/* Injected-draw arrays for the INJECT parity mode: row i holds the
+ * reference stream's draws k0 .. k0+K-1 of particle pid0+i, as raw 64-bit
+ * words and as reference normals (rng.py:45-66, :137-143). */
+void orc_fill_draws(uint64_t seed, uint64_t pid0, int64_t n, uint64_t k0, int64_t K,
+                    uint64_t *raw, double *nrm, int32_t n_threads) {
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t j = 0; j < K; ++j) {
+      uint64_t r = orc_raw64(seed, pid0 + (uint64_t)i, k0 + (uint64_t)j);
+      raw[i * K + j] = r;
+      nrm[i * K + j] = orc_u64_to_normal(r);
+    }
+  }
+}
+
+/* Same for per-row (seed, pid, k0) triples (per-step parity). */
+void orc_fill_draws_rows(const uint64_t *seed, const uint64_t *pid, const uint64_t *k0,
+                         int64_t n, int64_t K, uint64_t *raw, double *nrm) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < K; ++j) {
+      uint64_t r = orc_raw64(seed[i], pid[i], k0[i] + (uint64_t)j);
+      raw[i * K + j] = r;
+      nrm[i * K + j] = orc_u64_to_normal(r);
+    }
+}

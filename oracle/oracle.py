@@ -64,6 +64,8 @@ def lib():
                                         i64, P, P, P, P, i32]
         L.orc_histogram.argtypes = [i64, P, P, P, P, P, P]
         L.orc_max_threads.restype = C.c_int
+        L.orc_fill_draws.argtypes = [u64, u64, i64, u64, i64, P, P, i32]
+        L.orc_fill_draws_rows.argtypes = [P, P, P, i64, i64, P, P]
         _lib = L
     return _lib
 
@@ -183,3 +185,22 @@ def histogram(edges, positions, offsets, counts, dx):
 
 def max_threads():
     return int(lib().orc_max_threads())
+
+
+def fill_draws(seed, n, K, pid0=0, k0=0, threads=0):
+    """Reference-stream draws ``[n, K]`` (raw uint64, normals float64) for INJECT."""
+    raw = np.zeros((n, K), np.uint64)
+    nrm = np.zeros((n, K), np.float64)
+    lib().orc_fill_draws(seed, pid0, n, k0, K, _ptr(raw), _ptr(nrm), threads)
+    return raw, nrm
+
+
+def fill_draws_rows(seeds, pids, k0s, K):
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    pids = np.ascontiguousarray(pids, np.uint64)
+    k0s = np.ascontiguousarray(k0s, np.uint64)
+    n = seeds.shape[0]
+    raw = np.zeros((n, K), np.uint64)
+    nrm = np.zeros((n, K), np.float64)
+    lib().orc_fill_draws_rows(_ptr(seeds), _ptr(pids), _ptr(k0s), n, K, _ptr(raw), _ptr(nrm))
+    return raw, nrm

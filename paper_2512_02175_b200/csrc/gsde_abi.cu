@@ -1,0 +1,391 @@
+// gsde_abi.cu -- the extern "C" boundary (include/gsde.h): graph upload,
+// argument checks, stream/mode dispatch and host-side scalar helpers.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gsde_internal.h"
+
+namespace gsde {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int set_error(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+DevInfo dev_info(int device) {
+  static std::mutex mu;
+  static std::vector<DevInfo> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)cache.size() <= device) cache.resize(device + 1);
+  if (cache[device].sm_count == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cache[device].sm_count = v > 0 ? v : 1;
+  }
+  return cache[device];
+}
+
+namespace {
+
+// Scoped device switch (restores the caller's current device).
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return set_error(GSDE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// Vose alias table over one vertex's slot weights: column j keeps slot j
+// with probability prob[j], else jumps to alias[j].
+void build_alias(const double *w, int deg, std::vector<double> &prob, std::vector<int> &alias) {
+  prob.assign(deg, 1.0);
+  alias.resize(deg);
+  std::vector<double> p(deg);
+  std::vector<int> small, large;
+  double tot = 0.0;
+  for (int j = 0; j < deg; ++j) tot += w[j];
+  for (int j = 0; j < deg; ++j) {
+    alias[j] = j;
+    p[j] = tot > 0.0 ? w[j] / tot * deg : 1.0;
+    (p[j] < 1.0 ? small : large).push_back(j);
+  }
+  while (!small.empty() && !large.empty()) {
+    const int s = small.back();
+    small.pop_back();
+    const int l = large.back();
+    large.pop_back();
+    prob[s] = p[s];
+    alias[s] = l;
+    p[l] = (p[l] + p[s]) - 1.0;
+    (p[l] < 1.0 ? small : large).push_back(l);
+  }
+  for (int j : small) prob[j] = 1.0, alias[j] = j;
+  for (int j : large) prob[j] = 1.0, alias[j] = j;
+}
+
+struct Arena {
+  std::vector<unsigned char> host;
+  size_t add(const void *src, size_t bytes) {
+    const size_t off = (host.size() + 255) & ~size_t(255);
+    host.resize(off + (bytes ? bytes : 1));
+    if (bytes) memcpy(host.data() + off, src, bytes);
+    return off;
+  }
+};
+
+}  // namespace
+}  // namespace gsde
+
+using namespace gsde;
+
+extern "C" {
+
+int gsde_abi_version(void) { return GSDE_ABI_VERSION; }
+const char *gsde_last_error(void) { return g_last_error.c_str(); }
+int64_t gsde_launch_count(void) { return g_launches.load(); }
+
+uint64_t gsde_raw64(uint64_t seed, uint64_t stream, uint64_t index) {
+  return raw64(seed, stream, index);
+}
+double gsde_uniform01(uint64_t seed, uint64_t stream, uint64_t index) {
+  return u53_to_uniform(raw64(seed, stream, index) >> 11);
+}
+double gsde_normal(uint64_t seed, uint64_t stream, uint64_t index) {
+  return u64_to_normal(raw64(seed, stream, index));
+}
+double gsde_solve_first_passage_s(double a, double b, double c) {
+  return solve_first_passage_s<double>(a, b, c);
+}
+
+int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
+  if (!d || !out) return set_error(GSDE_EINVAL, "graph_create: null argument");
+  *out = nullptr;
+  const int64_t E = d->n_edges, V = d->n_vertices;
+  if (E < 1 || V < 1 || E > (1ll << 30) || V > (1ll << 30))
+    return set_error(GSDE_EINVAL, "graph_create: bad sizes E=%lld V=%lld", (long long)E,
+                     (long long)V);
+  const int64_t S = d->v_off[V];
+  const int64_t T = d->n_tab;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return set_error(GSDE_ENODEV, "graph_create: CUDA device %d unavailable", device);
+  DeviceGuard guard(device);
+  if (!guard.ok) return set_error(GSDE_ENODEV, "graph_create: cannot select device %d", device);
+
+  // --- host-side packing --------------------------------------------------
+  std::vector<int32_t> einit(E), eterm(E), voff(V + 1), vedges(S), taboff(E + 1);
+  std::vector<uint8_t> vorient(S), kind(E);
+  std::vector<uint64_t> thresh(S);
+  std::vector<double> len64(E), coef64(E), sig64(E), tabx64(T ? T : 1), tabmu64(T ? T : 1);
+  std::vector<float> len32(E), coef32(E), sig32(E), tabx32(T ? T : 1), tabmu32(T ? T : 1);
+  bool has_tab = false;
+  for (int64_t e = 0; e < E; ++e) {
+    einit[e] = (int32_t)d->edge_init[e];
+    eterm[e] = (int32_t)d->edge_term[e];
+    len64[e] = d->edge_length[e];
+    len32[e] = (float)d->edge_length[e];
+    kind[e] = (uint8_t)d->dkind[e];
+    coef64[e] = d->dcoef[e];
+    coef32[e] = (float)d->dcoef[e];
+    sig64[e] = d->sigma[e];
+    sig32[e] = (float)d->sigma[e];
+    if (kind[e] == 2) has_tab = true;
+    if (kind[e] > 2) return set_error(GSDE_EINVAL, "graph_create: bad drift kind on edge %lld",
+                                      (long long)e);
+  }
+  for (int64_t e = 0; e <= E; ++e) taboff[e] = (int32_t)d->tab_off[e];
+  for (int64_t t = 0; t < T; ++t) {
+    tabx64[t] = d->tab_x[t];
+    tabmu64[t] = d->tab_mu[t];
+    tabx32[t] = (float)d->tab_x[t];
+    tabmu32[t] = (float)d->tab_mu[t];
+  }
+  for (int64_t v = 0; v <= V; ++v) voff[v] = (int32_t)d->v_off[v];
+  const double two53 = 9007199254740992.0;
+  for (int64_t j = 0; j < S; ++j) {
+    vedges[j] = (int32_t)d->v_edges[j];
+    vorient[j] = (uint8_t)d->v_orient[j];
+    double c = std::floor(d->v_cumw[j] * two53);  // exact: scaling by 2^53
+    if (!(c > 0.0)) c = 0.0;
+    if (c > two53) c = two53;
+    thresh[j] = (uint64_t)c;
+  }
+  // native records
+  std::vector<float4> nedge(E);
+  std::vector<int4> nedgev(E), ncol(S);
+  for (int64_t e = 0; e < E; ++e) {
+    float4 r;
+    r.x = len32[e];
+    r.w = sig32[e];
+    if (kind[e] == 0) {
+      r.y = coef32[e];
+      r.z = 0.0f;
+    } else if (kind[e] == 1) {
+      r.y = 0.0f;
+      r.z = coef32[e];
+    } else {
+      int32_t off = taboff[e];
+      memcpy(&r.y, &off, sizeof(float));
+      r.z = NAN;
+    }
+    nedge[e] = r;
+    const int32_t a = einit[e], b = eterm[e];
+    nedgev[e] = make_int4(voff[a], voff[a + 1] - voff[a], b >= 0 ? voff[b] : 0,
+                          b >= 0 ? voff[b + 1] - voff[b] : 0);
+  }
+  std::vector<double> prob;
+  std::vector<int> alias;
+  for (int64_t v = 0; v < V; ++v) {
+    const int lo = voff[v], deg = voff[v + 1] - voff[v];
+    if (deg < 1) return set_error(GSDE_EINVAL, "graph_create: vertex %lld has no slots",
+                                  (long long)v);
+    build_alias(d->v_weights + lo, deg, prob, alias);
+    for (int j = 0; j < deg; ++j) {
+      const int sp = lo + j, sa = lo + alias[j];
+      const uint32_t prim = (uint32_t)vedges[sp] | ((uint32_t)vorient[sp] << 31);
+      const uint32_t alt = (uint32_t)vedges[sa] | ((uint32_t)vorient[sa] << 31);
+      double t = std::nearbyint(prob[j] * 4294967296.0);
+      uint32_t th = t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)(t > 0.0 ? t : 0.0);
+      int4 c;
+      c.x = (int)th;
+      c.y = (int)prim;
+      c.z = (int)(prob[j] >= 1.0 ? prim : alt);
+      c.w = 0;
+      ncol[sp] = c;
+    }
+  }
+
+  Arena A;
+  const size_t o_len64 = A.add(len64.data(), E * 8), o_coef64 = A.add(coef64.data(), E * 8),
+               o_sig64 = A.add(sig64.data(), E * 8), o_tabx64 = A.add(tabx64.data(), tabx64.size() * 8),
+               o_tabmu64 = A.add(tabmu64.data(), tabmu64.size() * 8),
+               o_len32 = A.add(len32.data(), E * 4), o_coef32 = A.add(coef32.data(), E * 4),
+               o_sig32 = A.add(sig32.data(), E * 4), o_tabx32 = A.add(tabx32.data(), tabx32.size() * 4),
+               o_tabmu32 = A.add(tabmu32.data(), tabmu32.size() * 4),
+               o_einit = A.add(einit.data(), E * 4), o_eterm = A.add(eterm.data(), E * 4),
+               o_voff = A.add(voff.data(), (V + 1) * 4), o_vedges = A.add(vedges.data(), S * 4),
+               o_vorient = A.add(vorient.data(), S), o_thresh = A.add(thresh.data(), S * 8),
+               o_kind = A.add(kind.data(), E), o_taboff = A.add(taboff.data(), (E + 1) * 4),
+               o_nedge = A.add(nedge.data(), E * sizeof(float4)),
+               o_nedgev = A.add(nedgev.data(), E * sizeof(int4)),
+               o_ncol = A.add(ncol.data(), S * sizeof(int4));
+  void *dev = nullptr;
+  cudaError_t err = cudaMalloc(&dev, A.host.size());
+  if (err != cudaSuccess) return set_error(GSDE_ENOMEM, "graph_create: cudaMalloc(%zu): %s",
+                                           A.host.size(), cudaGetErrorString(err));
+  err = cudaMemcpy(dev, A.host.data(), A.host.size(), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(dev);
+    return cuda_fail(err, "graph_create: upload");
+  }
+  auto P = [&](size_t off) { return (void *)((unsigned char *)dev + off); };
+  gsde_graph *g = new gsde_graph();
+  g->device = device;
+  g->E = E;
+  g->V = V;
+  g->S = S;
+  g->T = T;
+  g->is_star = d->is_star != 0;
+  g->has_tab = has_tab;
+  g->arena = dev;
+  g->arena_bytes = (int64_t)A.host.size();
+  auto fill_ref = [&](auto &R, size_t ol, size_t oc, size_t os, size_t ox, size_t om) {
+    using T_ = std::remove_pointer_t<decltype(R.edge_len)>;
+    R.n_edges = (int32_t)E;
+    R.edge_len = (const T_ *)P(ol);
+    R.dcoef = (const T_ *)P(oc);
+    R.sigma = (const T_ *)P(os);
+    R.tab_x = (const T_ *)P(ox);
+    R.tab_mu = (const T_ *)P(om);
+    R.edge_init = (const int32_t *)P(o_einit);
+    R.edge_term = (const int32_t *)P(o_eterm);
+    R.v_off = (const int32_t *)P(o_voff);
+    R.v_edges = (const int32_t *)P(o_vedges);
+    R.v_orient = (const uint8_t *)P(o_vorient);
+    R.v_thresh = (const uint64_t *)P(o_thresh);
+    R.dkind = (const uint8_t *)P(o_kind);
+    R.tab_off = (const int32_t *)P(o_taboff);
+  };
+  fill_ref(g->ref64, o_len64, o_coef64, o_sig64, o_tabx64, o_tabmu64);
+  fill_ref(g->ref32, o_len32, o_coef32, o_sig32, o_tabx32, o_tabmu32);
+  g->nat.n_edges = (int32_t)E;
+  g->nat.n_slots = (int32_t)S;
+  g->nat.edge = (const float4 *)P(o_nedge);
+  g->nat.edgev = (const int4 *)P(o_nedgev);
+  g->nat.col = (const int4 *)P(o_ncol);
+  g->nat.tab_off = (const int32_t *)P(o_taboff);
+  g->nat.tab_x = (const float *)P(o_tabx32);
+  g->nat.tab_mu = (const float *)P(o_tabmu32);
+  g->nat.has_tab = has_tab ? 1 : 0;
+  const int64_t stage = E * (g->is_star ? 16 : 32) + S * 16;
+  g->nat_graph_smem = stage <= 32 * 1024 ? stage : 0;
+  *out = g;
+  return GSDE_OK;
+}
+
+int gsde_graph_destroy(gsde_graph *g) {
+  if (!g) return GSDE_OK;
+  DeviceGuard guard(g->device);
+  cudaError_t err = cudaFree(g->arena);
+  delete g;
+  return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "graph_destroy");
+}
+
+int64_t gsde_graph_device_bytes(const gsde_graph *g) { return g ? g->arena_bytes : 0; }
+
+static int check_stream_args(int32_t stream, int32_t precision, const uint64_t *inj_raw,
+                             const double *inj_normal, int64_t inj_stride, const char *who) {
+  if (stream != GSDE_STREAM_NATIVE && stream != GSDE_STREAM_REFERENCE &&
+      stream != GSDE_STREAM_INJECT)
+    return set_error(GSDE_EINVAL, "%s: unknown stream mode %d", who, stream);
+  if (stream == GSDE_STREAM_INJECT) {
+    if (!inj_raw || !inj_normal || inj_stride < 1)
+      return set_error(GSDE_EINVAL, "%s: INJECT needs inj_raw, inj_normal and inj_stride", who);
+    if (precision != GSDE_PREC_F32 && precision != GSDE_PREC_F64)
+      return set_error(GSDE_EINVAL, "%s: unknown precision %d", who, precision);
+  }
+  return GSDE_OK;
+}
+
+int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, void *stream) {
+  if (!g || !a || !o) return set_error(GSDE_EINVAL, "ensemble: null argument");
+  if (a->n_particles < 0 || a->n_steps < 0)
+    return set_error(GSDE_EINVAL, "ensemble: n_steps and n_particles must be nonnegative");
+  if (!(a->dt > 0.0) || !std::isfinite(a->dt))
+    return set_error(GSDE_EINVAL, "ensemble: dt must be positive and finite");
+  if (a->cap < 1) return set_error(GSDE_EINVAL, "ensemble: cap must be >= 1");
+  if (a->reflect_len < 0.0 || (a->reflect_len > 0.0 && !g->is_star))
+    return set_error(GSDE_EINVAL, "ensemble: reflect_len applies to star graphs only");
+  if (a->init_kind != GSDE_INIT_POINT && a->init_kind != GSDE_INIT_PER_EDGE_UNIFORM)
+    return set_error(GSDE_EINVAL, "ensemble: bad init_kind %d", a->init_kind);
+  if (a->init_kind == GSDE_INIT_POINT && (a->init_edge < 0 || a->init_edge >= g->E))
+    return set_error(GSDE_EINVAL, "ensemble: init_edge out of range");
+  if (o->hist && (!o->hist_offsets || !o->hist_counts || !o->hist_dx))
+    return set_error(GSDE_EINVAL, "ensemble: hist needs offsets, counts and dx");
+  int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
+                             "ensemble");
+  if (rc) return rc;
+  if (a->stream == GSDE_STREAM_NATIVE && a->n_steps > 0x7fffffffll)
+    return set_error(GSDE_EINVAL, "ensemble: NATIVE stream supports n_steps < 2^31");
+  if (a->n_particles == 0) return GSDE_OK;
+  DeviceGuard guard(g->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  const cudaError_t err = a->stream == GSDE_STREAM_NATIVE ? launch_native_ensemble(g, *a, *o, s)
+                                                          : launch_ref_ensemble(g, *a, *o, s);
+  return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "ensemble launch");
+}
+
+int gsde_vertex_trials(const gsde_graph *g, const gsde_trials *a, const gsde_trials_out *o,
+                       void *stream) {
+  if (!g || !a || !o) return set_error(GSDE_EINVAL, "vertex_trials: null argument");
+  if (a->n_trials < 0) return set_error(GSDE_EINVAL, "vertex_trials: n_trials must be >= 0");
+  if (!(a->dt > 0.0)) return set_error(GSDE_EINVAL, "vertex_trials: dt must be positive");
+  if (a->cap < 1) return set_error(GSDE_EINVAL, "vertex_trials: cap must be >= 1");
+  if (!g->is_star && (a->start_edge < 0 || a->start_edge >= g->E))
+    return set_error(GSDE_EINVAL, "vertex_trials: start_edge out of range");
+  int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
+                             "vertex_trials");
+  if (rc) return rc;
+  if (a->n_trials == 0) return GSDE_OK;
+  DeviceGuard guard(g->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  const cudaError_t err = a->stream == GSDE_STREAM_NATIVE ? launch_native_trials(g, *a, *o, s)
+                                                          : launch_ref_trials(g, *a, *o, s);
+  return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "vertex_trials launch");
+}
+
+int gsde_step_batch(const gsde_graph *g, const gsde_step_args *a, int64_t *edge, double *x,
+                    uint64_t *k, int64_t *M, int64_t *trunc, void *stream) {
+  if (!g || !a || !edge || !x || !k) return set_error(GSDE_EINVAL, "step_batch: null argument");
+  if (a->n < 0 || !(a->dt > 0.0) || a->cap < 1)
+    return set_error(GSDE_EINVAL, "step_batch: bad n / dt / cap");
+  if (a->stream == GSDE_STREAM_NATIVE)
+    return set_error(GSDE_EINVAL, "step_batch: REFERENCE or INJECT streams only");
+  if (a->stream == GSDE_STREAM_REFERENCE && (!a->seed || !a->pid))
+    return set_error(GSDE_EINVAL, "step_batch: REFERENCE needs seed and pid arrays");
+  int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
+                             "step_batch");
+  if (rc) return rc;
+  DeviceGuard guard(g->device);
+  const cudaError_t err = launch_step_batch(g, *a, edge, x, k, M, trunc, (cudaStream_t)stream);
+  return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "step_batch launch");
+}
+
+int gsde_histogram(int64_t n, const int64_t *edge, const double *x, const int64_t *offsets,
+                   const int64_t *counts, const double *dx, int64_t n_cells, int64_t *hist,
+                   void *stream) {
+  if (n < 0 || n_cells < 1 || (n > 0 && (!edge || !x)) || !offsets || !counts || !dx || !hist)
+    return set_error(GSDE_EINVAL, "histogram: bad arguments");
+  const cudaError_t err =
+      launch_histogram(n, edge, x, offsets, counts, dx, n_cells, hist, (cudaStream_t)stream);
+  return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "histogram launch");
+}
+
+}  // extern "C"

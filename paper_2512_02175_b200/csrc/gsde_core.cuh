@@ -1,0 +1,192 @@
+// gsde_core.cuh -- shared host/device building blocks of the simulator.
+//
+//  * Philox4x32-10 and the reference's (seed, stream, index) -> 64-bit draw
+//    layout (reference rng.py:29-66);
+//  * 53-bit uniforms and the AS241 normal quantile on the centred lattice
+//    (rng.py:69-143), evaluated on exact (q, min(p,1-p)) pairs;
+//  * the first-passage quadratic (kernels.py:88-131), templated on the real type;
+//  * device-side graph views.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define GSDE_HD __host__ __device__ __forceinline__
+#else
+#define GSDE_HD inline
+#endif
+
+namespace gsde {
+
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+struct Block {
+  uint32_t x, y, z, w;
+};
+
+// 10 rounds; each round: two 32x32->64 products (one IMAD.WIDE each on the
+// device), two 3-input xors (LOP3), key bump (uniform across the warp).
+GSDE_HD Block philox4x32_10(Block c, uint32_t k0, uint32_t k1) {
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c.x;
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * c.z;
+    Block n;
+    n.x = (uint32_t)(p1 >> 32) ^ c.y ^ k0;
+    n.y = (uint32_t)p1;
+    n.z = (uint32_t)(p0 >> 32) ^ c.w ^ k1;
+    n.w = (uint32_t)p0;
+    c = n;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  return c;
+}
+
+// Reference stream layout (rng.py:45-66): block index = draw >> 1 in counter
+// words 0-1, stream (particle) in words 2-3, seed as key; even draw -> words
+// (0,1), odd draw -> words (2,3), high word first.
+GSDE_HD Block ref_block(uint64_t seed, uint64_t stream, uint64_t blk) {
+  Block c{(uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+  return philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+GSDE_HD uint64_t ref_half(const Block &b, uint64_t index) {
+  return (index & 1u) ? (((uint64_t)b.z << 32) | b.w) : (((uint64_t)b.x << 32) | b.y);
+}
+
+GSDE_HD uint64_t raw64(uint64_t seed, uint64_t stream, uint64_t index) {
+  return ref_half(ref_block(seed, stream, index >> 1), index);
+}
+
+constexpr double kInv2p53 = 1.0 / 9007199254740992.0;
+
+// rng.py:69-72
+GSDE_HD double u53_to_uniform(uint64_t n53) { return (double)n53 * kInv2p53; }
+
+// rng.py:81-134 (AS241), on q = p - 1/2 and pt = min(p, 1 - p).
+GSDE_HD double norm_ppf_qt(double q, double pt) {
+  if (fabs(q) <= 0.425) {
+    const double r = 0.180625 - q * q;
+    const double num = (((((((2.5090809287301226727e3 * r + 3.3430575583588128105e4) * r +
+                             6.7265770927008700853e4) * r + 4.5921953931549871457e4) * r +
+                           1.3731693765509461125e4) * r + 1.9715909503065514427e3) * r +
+                         1.3314166789178437745e2) * r + 3.3871328727963666080e0);
+    const double den = (((((((5.2264952788528545610e3 * r + 2.8729085735721942674e4) * r +
+                             3.9307895800092710610e4) * r + 2.1213794301586595867e4) * r +
+                           5.3941960214247511077e3) * r + 6.8718700749205790830e2) * r +
+                         4.2313330701600911252e1) * r + 1.0);
+    return q * num / den;
+  }
+  const double r = sqrt(-log(pt));
+  if (r <= 5.0) {
+    const double rr = r - 1.6;
+    const double num = (((((((7.74545014278341407640e-4 * rr + 2.27238449892691845833e-2) * rr +
+                             2.41780725177450611770e-1) * rr + 1.27045825245236838258e0) * rr +
+                           3.64784832476320460504e0) * rr + 5.76949722146069140550e0) * rr +
+                         4.63033784615654529590e0) * rr + 1.42343711074968357734e0);
+    const double den = (((((((1.05075007164441684324e-9 * rr + 5.47593808499534494600e-4) * rr +
+                             1.51986665636164571966e-2) * rr + 1.48103976427480074590e-1) * rr +
+                           6.89767334985100004550e-1) * rr + 1.67638483018380384940e0) * rr +
+                         2.05319162663775882187e0) * rr + 1.0);
+    const double val = num / den;
+    return q < 0.0 ? -val : val;
+  }
+  const double rr = r - 5.0;
+  const double num = (((((((2.01033439929228813265e-7 * rr + 2.71155556874348757815e-5) * rr +
+                           1.24266094738807843860e-3) * rr + 2.65321895265761230930e-2) * rr +
+                         2.96560571828504891230e-1) * rr + 1.78482653991729133580e0) * rr +
+                       5.46378491116411436990e0) * rr + 6.65790464350110377720e0);
+  const double den = (((((((2.04426310338993978564e-15 * rr + 1.42151175831644588870e-9) * rr +
+                           1.84631831751005468180e-6) * rr + 7.86869131145613259100e-4) * rr +
+                         1.48753612908506148525e-2) * rr + 1.36929880922735805310e-1) * rr +
+                       5.99832206555887937690e-1) * rr + 1.0);
+  double x = -(num / den);
+  for (int i = 0; i < 2; ++i) {  // Newton polish against erfc (rng.py:124-131)
+    const double cdf = 0.5 * erfc(-x / 1.4142135623730951);
+    const double pdf = 0.3989422804014327 * exp(-0.5 * x * x);
+    x -= (cdf - pt) / pdf;
+  }
+  return q < 0.0 ? x : -x;
+}
+
+// rng.py:137-143: p = (n + 1/2) 2^-53; q and min(p, 1-p) formed exactly.
+GSDE_HD double u64_to_normal(uint64_t r) {
+  const int64_t n = (int64_t)(r >> 11);
+  const double q = ((double)(n - 4503599627370496LL) + 0.5) * kInv2p53;
+  const double pt = q < 0.0 ? ((double)n + 0.5) * kInv2p53
+                            : ((double)(9007199254740992LL - n) - 0.5) * kInv2p53;
+  return norm_ppf_qt(q, pt);
+}
+
+// kernels.py:88-131: first s >= 0 where a s^2 + b s + c crosses zero, clamped
+// to [0, 1]; -1 if no crossing.
+template <class R>
+GSDE_HD R solve_first_passage_s(R a, R b, R c) {
+  const R zero = R(0), one = R(1);
+  if (c < zero) return zero;
+  if (c == zero) {
+    if (b <= zero) return zero;
+    if (a >= zero) return -one;
+    const R s = -b / a;
+    return s < one ? s : one;
+  }
+  if (a == zero) {
+    if (b >= zero) return -one;
+    const R s = -c / b;
+    return s < one ? s : one;
+  }
+  R disc = b * b - R(4) * a * c;
+  if (disc < zero) disc = zero;
+  const R sq = sqrt(disc);
+  const R q = b >= zero ? R(-0.5) * (b + sq) : R(-0.5) * (b - sq);
+  R s = -one;
+  const R r1 = q / a;
+  if (r1 >= zero) s = r1;
+  if (q != zero) {
+    const R r2 = c / q;
+    if (r2 >= zero && (s < zero || r2 < s)) s = r2;
+  }
+  if (s < zero) return -one;
+  return s < one ? s : one;
+}
+
+// ---------------------------------------------------------------------------
+// Device graph views.
+
+// Reference-layout view (REFERENCE / INJECT streams), real type R.
+template <class R>
+struct RefGraph {
+  int32_t n_edges;
+  const R *edge_len;
+  const int32_t *edge_init, *edge_term;
+  const int32_t *v_off, *v_edges;
+  const uint8_t *v_orient;
+  const uint64_t *v_thresh;  // floor(cumw * 2^53), saturated
+  const uint8_t *dkind;
+  const R *dcoef;
+  const int32_t *tab_off;
+  const R *tab_x, *tab_mu, *sigma;
+};
+
+// Native records (FP32 stream).
+//   edge:  {len, mu_a, mu_b, sigma}: mu(x) = mu_a + mu_b x; mu_b = NaN marks a
+//          tabulated edge whose table starts at __float_as_int(mu_a).
+//   edgev: {init_off, init_deg, term_off, term_deg} of the endpoint vertices'
+//          alias columns (term_deg = 0 at the vertex at infinity).
+//   col:   alias column {thresh, prim, alias, 0}; prim/alias = edge | orient<<31.
+struct NativeGraph {
+  int32_t n_edges, n_slots;
+  const float4 *edge;
+  const int4 *edgev;
+  const int4 *col;
+  const int32_t *tab_off;
+  const float *tab_x, *tab_mu;
+  int32_t has_tab;
+};
+
+}  // namespace gsde

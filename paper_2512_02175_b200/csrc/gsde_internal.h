@@ -1,0 +1,52 @@
+// gsde_internal.h -- declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gsde.h"
+#include "gsde_core.cuh"
+
+struct gsde_graph_s {
+  int device = 0;
+  int64_t E = 0, V = 0, S = 0, T = 0;
+  bool is_star = false;
+  bool has_tab = false;
+  void *arena = nullptr;
+  int64_t arena_bytes = 0;
+  gsde::RefGraph<double> ref64{};
+  gsde::RefGraph<float> ref32{};
+  gsde::NativeGraph nat{};
+  // native smem staging size for the whole graph (0 = too large, read via L2)
+  int64_t nat_graph_smem = 0;
+};
+
+namespace gsde {
+
+// Per-call device properties (cached per device).
+struct DevInfo {
+  int sm_count = 0;
+};
+DevInfo dev_info(int device);
+
+void count_launch(int n = 1);
+int set_error(int code, const char *fmt, ...);
+
+// gsde_ref.cu (FP64 / injected streams; strict IEEE, no FMA contraction)
+cudaError_t launch_ref_ensemble(const gsde_graph *g, const gsde_run &a, const gsde_out &o,
+                                cudaStream_t s);
+cudaError_t launch_ref_trials(const gsde_graph *g, const gsde_trials &a,
+                              const gsde_trials_out &o, cudaStream_t s);
+cudaError_t launch_step_batch(const gsde_graph *g, const gsde_step_args &a, int64_t *edge,
+                              double *x, uint64_t *k, int64_t *M, int64_t *trunc,
+                              cudaStream_t s);
+
+// gsde_native.cu (FP32 production stream)
+cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const gsde_out &o,
+                                   cudaStream_t s);
+cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
+                                 const gsde_trials_out &o, cudaStream_t s);
+cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,
+                             const int64_t *offsets, const int64_t *counts, const double *dx,
+                             int64_t n_cells, int64_t *hist, cudaStream_t s);
+
+}  // namespace gsde

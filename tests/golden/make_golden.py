@@ -259,8 +259,31 @@ def stat_vectors(ens):
     )
 
 
+def graph_vectors():
+    """Packed arrays + gamma of every case as built by the reference."""
+    out = {}
+    vtext = vascular_small()
+    for case in list(CASES) + ["vascular_small"]:
+        if case == "vascular_small":
+            g, f = graphfile.parse_graph_file(vtext)
+        else:
+            g, f = build(case, gs)
+        kind, coef, tab_off, tab_x, tab_mu, sigma = f.packed()
+        out[case] = dict(edge_init=g.edge_init, edge_term=g.edge_term, edge_length=g.edge_length,
+                         v_off=g.v_off, v_edges=g.v_edges, v_orient=g.v_orient, v_cumw=g.v_cumw,
+                         is_star=np.array([g.is_star]), dkind=kind, dcoef=coef, tab_off=tab_off,
+                         tab_x=tab_x, tab_mu=tab_mu, sigma=sigma,
+                         graph_gamma=np.array([engine._graph_gamma(g, f, 1e-3)]))
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
+    gv = graph_vectors()
+    np.savez_compressed(os.path.join(HERE, "graphs.npz"),
+                        **{f"{c}/{k}": v for c, d in gv.items() for k, v in d.items()})
+    if "--only-graphs" in sys.argv:
+        return
     with open(os.path.join(HERE, "rng.json"), "w") as fh:
         json.dump(rng_vectors(), fh, indent=0)
     with open(os.path.join(HERE, "solvers.json"), "w") as fh:

@@ -1,0 +1,221 @@
+"""GPU native (FP32 production) stream: statistical parity + invariants.
+
+The native stream is not bit-comparable to the reference, so it is held to
+the north-star's Monte Carlo contract: exit probabilities within binomial
+standard errors (Bonferroni-corrected 4 sigma) of the REFERENCE stream run at
+the same dt (which is itself pinned bit-exactly to the reference), binned
+densities by a two-sample chi-square / KS test, the chi-squared crossing law
+and Thm 3.1 bound, the paper's steady-state L2 targets (SPEC acceptance 5, 6,
+11) and size-independent invariants at full benchmark sizes.
+"""
+
+import numpy as np
+import pytest
+import torch
+from scipy import stats
+
+import cases
+import helpers
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import analysis, engine, workloads
+
+pytestmark = pytest.mark.gpu
+Z_MAX = 4.5  # Bonferroni over <= 50 comparisons at ~1e-5 family-wise
+
+
+@pytest.mark.parametrize("dt", [1e-2, 1e-3, 1e-4, 1e-5])
+def test_exit_probabilities_native_vs_reference_stream(dt):
+    g, f = cases.build("star5_linear", gs)
+    n = 2_000_000
+    nat = analysis.vertex_exit_counts(g, f, dt, n, seed=11, rng="native")
+    ref = analysis.vertex_exit_counts(g, f, dt, n, seed=12, rng="reference")
+    assert nat.counts.sum() == n and ref.counts.sum() == n
+    z = helpers.binom_z(nat.counts, n, ref.counts, n)
+    assert np.all(np.abs(z) < Z_MAX), (dt, z, nat.counts / n, ref.counts / n)
+    # mean number of crossings per trial agrees too
+    m_nat = nat.crossings_total / n
+    m_ref = ref.crossings_total / n
+    sd = np.sqrt(np.dot(np.arange(nat.m_histogram.size) ** 2, nat.m_histogram) / n - m_nat**2)
+    assert abs(m_nat - m_ref) < Z_MAX * sd * np.sqrt(2.0 / n)
+
+
+def test_exit_probability_experiment_convergence():
+    """Cor 3.3 / SPEC acceptance 4 at 1e6 trials per dt."""
+    g, f = cases.build("star5_linear", gs)
+    rep = analysis.exit_probability_experiment(g, f, [1e-2, 1e-3, 1e-4], 1_000_000, 11)
+    assert rep.nonincreasing
+    last = rep.rows[-1]
+    assert np.all(np.abs(last.frequencies - 0.2) < 4 * last.binomial_se + 0.01)
+
+
+def test_driftless_exit_frequencies_are_the_weights():
+    g, f = cases.build("star4_mixed", gs)
+    f0 = gs.CoefficientField.for_graph(g, [gs.ConstantDrift(0.0)] * 4, [1.0] * 4)
+    n = 4_000_000
+    ec = analysis.vertex_exit_counts(g, f0, 1e-3, n, seed=3)
+    w = np.array([0.1, 0.0, 0.6, 0.3])
+    assert ec.counts[1] == 0  # zero-weight edge never taken
+    se = np.sqrt(w * (1 - w) / n) + 1e-12
+    assert np.all(np.abs(ec.counts / n - w) < Z_MAX * se)
+    assert ec.m_histogram[1] == n  # mu = 0 -> M == 1 always (SPEC em_step_star example)
+
+
+@pytest.mark.parametrize("rng", ["native", "reference"])
+def test_chi2_crossing_law_and_bound(rng):
+    """SPEC acceptance 2 + 3: homogeneous star, P(M <= k) = P(chi2_k >= gamma)."""
+    g, f = cases.build("star_homog", gs)
+    for dt, n in ((1e-3, 2_000_000), (2e-4, 1_000_000), (4e-3, 1_000_000)):
+        tr = analysis.vertex_exit_counts(g, f, dt, n, seed=5, rng=rng)
+        bst = gs.BounceStats(tr.m_histogram, tr.gamma, tr.truncation_count, tr.crossings_total,
+                             tr.crossing_events)
+        rep = analysis.check_crossing_bound(bst)
+        assert not rep.any_bound_violation
+        for row in rep.rows:
+            assert abs(row.empirical - row.chi2_tail) < Z_MAX * max(row.std_error, 1e-9), row
+
+
+def test_density_native_vs_reference_stream_c2():
+    """C2 geometry at 1e6 particles: binned densities agree (two-sample chi2 + KS)."""
+    g, f = workloads.hub64()
+    grid = gs.EdgeGrid.uniform(g, 8)
+    mk = lambda rng, seed: gs.SimulationConfig(dt=1e-3, n_steps=300, n_particles=1_000_000,
+                                               seed=seed, initial=gs.PerEdgeUniform(2.0), rng=rng)
+    hn, sn = analysis.run_ensemble_histogram(g, f, mk("native", 1), grid)
+    hr, sr = analysis.run_ensemble_histogram(g, f, mk("reference", 2), grid)
+    p, chi2, dof = helpers.chi2_two_sample(hn.counts, hr.counts)
+    assert p > 1e-4, (p, chi2, dof)
+    rn = gs.run_ensemble(g, f, mk("native", 3))
+    rr = gs.run_ensemble(g, f, mk("reference", 4))
+    for e in (0, 17, 63):
+        ks = stats.ks_2samp(rn.positions[rn.edges == e], rr.positions[rr.edges == e])
+        assert ks.pvalue > 1e-4, (e, ks)
+    en = rn.stats.crossings_total / 3e8
+    er = rr.stats.crossings_total / 3e8
+    assert abs(en - er) < 0.02 * er
+
+
+def test_c1_exit_fractions_and_density():
+    """C1 (3-edge Brownian star): final-edge fractions are 1/3 and the native
+    density matches the reference stream."""
+    g, f = cases.build("star3_bm", gs)
+    n = 1_000_000
+    grid = gs.EdgeGrid.uniform(g, 16, lengths=[3.0] * 3)
+    cfg = lambda rng, s: gs.SimulationConfig(dt=1e-3, n_steps=1000, n_particles=n, seed=s, rng=rng)
+    hn, _ = analysis.run_ensemble_histogram(g, f, cfg("native", 1), grid)
+    hr, _ = analysis.run_ensemble_histogram(g, f, cfg("reference", 2), grid)
+    occ = hn.counts.reshape(3, 16).sum(1)
+    assert np.all(np.abs(occ / n - 1 / 3) < Z_MAX * np.sqrt(2 / 9 / n))
+    p, _, _ = helpers.chi2_two_sample(hn.counts, hr.counts)
+    assert p > 1e-4
+
+
+@pytest.mark.parametrize("kind", ["linear", "quadratic"])
+def test_steady_state_l2_paper_section_4_1(kind):
+    """SPEC acceptance 5/6: 1e6 particles, dt = 1e-4, T = 10, 200 bins per edge."""
+    g, f = workloads.star5(kind)
+    oracle = analysis.SteadyStateOracle.from_field(g, f)
+    grid = gs.EdgeGrid.uniform(g, 200, lengths=oracle.truncation_lengths(1e-8))
+    cfg = gs.SimulationConfig(dt=1e-4, n_steps=100_000, n_particles=1_000_000, seed=42)
+    h, st = analysis.run_ensemble_histogram(g, f, cfg, grid)
+    err = analysis.l2_error(h, oracle)
+    assert err < 0.05, err
+    assert st.truncation_count == 0
+
+
+def test_reflected_brownian_motion_uniform():
+    """SPEC acceptance 11: single finite edge, mu = 0 -> uniform, L2 < 0.02."""
+    g, f = cases.build("single_edge", gs)
+    grid = gs.EdgeGrid.uniform(g, 64)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=3000, n_particles=1_000_000, seed=8)
+    h, _ = analysis.run_ensemble_histogram(g, f, cfg, grid)
+    err = analysis.l2_error(h, lambda e, x: np.ones_like(x))
+    assert err < 0.02, err
+
+
+def test_native_determinism_and_sharding():
+    g, f = workloads.hub64()
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=100, n_particles=100_003, seed=21,
+                              initial=gs.PerEdgeUniform(2.0))
+    a = engine.ensemble_device(g, f, cfg)
+    b = engine.ensemble_device(g, f, cfg)
+    for k in ("edge", "x", "crossings", "m_hist", "totals"):
+        assert torch.equal(a[k], b[k]), k
+    parts = [engine.ensemble_device(g, f, cfg, pid_offset=o, n_particles=c)
+             for o, c in ((0, 50_000), (50_000, 50_003))]
+    for k in ("edge", "x", "crossings"):
+        assert torch.equal(a[k], torch.cat([p[k] for p in parts])), k
+    assert torch.equal(a["m_hist"], parts[0]["m_hist"] + parts[1]["m_hist"])
+
+
+@pytest.mark.parametrize("rng", ["native", "reference"])
+def test_full_size_invariants_c1_throughput(rng):
+    """C1 throughput size (1.6e7 x 1e3 native; 2e6 x 1e3 reference): the fused
+    estimators are mutually consistent and complete."""
+    g, f = cases.build("star3_bm", gs)
+    n = 16_000_000 if rng == "native" else 2_000_000
+    grid = gs.EdgeGrid.uniform(g, 16, lengths=[3.0] * 3)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=1000, n_particles=n, seed=20251202, rng=rng)
+    out = engine.ensemble_device(g, f, cfg, outputs=("edge_counts",), grid=grid)
+    mh = out["m_hist"].cpu().numpy()
+    tot = out["totals"].cpu().numpy()
+    assert int(out["hist"].sum()) == n
+    assert int(out["edge_counts"].sum()) == n
+    assert int(mh.sum()) == int(tot[1])                      # events
+    assert int((np.arange(mh.size) * mh).sum()) == int(tot[0])  # crossings
+    assert int(tot[2]) == 0
+    occ = out["edge_counts"].cpu().numpy() / n
+    assert np.all(np.abs(occ - 1 / 3) < Z_MAX * np.sqrt(2 / 9 / n))
+
+
+def test_vascular_invariants_and_density():
+    g, f = workloads.vascular(20_000, seed=4)
+    grid = gs.EdgeGrid.uniform(g, 4)
+    xmax = float(g.edge_length.max())
+    mk = lambda rng, s, n: gs.SimulationConfig(dt=1e-3, n_steps=100, n_particles=n, seed=s,
+                                               initial=gs.PerEdgeUniform(xmax), rng=rng)
+    hn, sn = analysis.run_ensemble_histogram(g, f, mk("native", 1, 4_000_000), grid)
+    hr, sr = analysis.run_ensemble_histogram(g, f, mk("reference", 2, 4_000_000), grid)
+    assert hn.counts.sum() == 4_000_000
+    # per-edge occupancy (coarse: 4 cells) agrees
+    p, chi2, dof = helpers.chi2_two_sample(hn.counts.reshape(-1, 4).sum(1),
+                                           hr.counts.reshape(-1, 4).sum(1))
+    assert p > 1e-4, (p, chi2, dof)
+    assert abs(sn.crossings_total - sr.crossings_total) < 0.01 * sr.crossings_total
+
+
+def test_per_trial_outputs_agree_with_fused_counts():
+    g, f = cases.build("hub8", gs)
+    tr = gs.vertex_crossing_trials(g, f, 1e-2, 300_000, 5)
+    ec = analysis.vertex_exit_counts(g, f, 1e-2, 300_000, 5)
+    np.testing.assert_array_equal(np.bincount(tr.exit_edges, minlength=8), ec.counts)
+    np.testing.assert_array_equal(tr.stats().m_histogram,
+                                  ec.m_histogram[: tr.stats().m_histogram.size])
+
+
+def test_edge_cases():
+    g, f = cases.build("star5_quad", gs)
+    # zero steps: placement only
+    r = gs.run_ensemble(g, f, gs.SimulationConfig(dt=1e-3, n_steps=0, n_particles=1000, seed=1,
+                                                  initial=gs.PerEdgeUniform(0.3)))
+    assert np.all((r.positions >= 0) & (r.positions <= 0.3))
+    assert r.crossings.sum() == 0 and r.stats.m_histogram.sum() == 0
+    # one particle, ragged sizes
+    for n in (1, 31, 33, 257, 4097):
+        r = gs.run_ensemble(g, f, gs.SimulationConfig(dt=1e-3, n_steps=50, n_particles=n, seed=2))
+        assert r.edges.shape == (n,) and np.all(r.positions >= 0)
+    # cap = 1 truncates at strongly repelling vertex
+    gc, fc = cases.build("star_homog", gs)
+    r = gs.run_ensemble(gc, fc, gs.SimulationConfig(dt=1e-2, n_steps=20, n_particles=20_000,
+                                                    seed=3, max_splits_per_step=1))
+    assert r.stats.truncation_count > 0
+    assert r.stats.m_histogram[1] == r.stats.crossing_events
+    # general graph, start exactly at the far end of an edge
+    gp, fp = cases.build("path3", gs)
+    r = gs.run_ensemble(gp, fp, gs.SimulationConfig(dt=1e-3, n_steps=10, n_particles=1000,
+                                                    seed=4, initial=gs.PointStart(1, 2.0)))
+    assert np.all((r.positions >= 0) & (r.positions <= gp.edge_length[r.edges]))
+    # reflect_at wall on a star (native)
+    r = gs.run_ensemble(g, f, gs.SimulationConfig(dt=1e-3, n_steps=100, n_particles=10_000,
+                                                  seed=5, reflect_at=0.05,
+                                                  initial=gs.PerEdgeUniform(0.05)))
+    assert np.all(r.positions <= 0.05)

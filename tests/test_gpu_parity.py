@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path vs the reference's golden outputs and the C oracle.
+
+* REFERENCE stream (FP64, the reference's own Philox/AS241 draws): edge ids,
+  crossing counts, crossing events, M histograms, truncations and draw
+  counters EXACT; positions within POS_ATOL = 1e-10 (reference is numba
+  fastmath; measured max ~1e-11 over hundreds of steps).
+* INJECT-f64 (oracle-made reference draws injected) == REFERENCE bit-for-bit.
+* INJECT-f32 (north-star contract): per step, restarted from the reference
+  state, edge/M exact and |dx| <= 1e-5 max(|x|, sigma sqrt(dt)); whole FP32
+  trajectories are reported as fractions (FP32 rounding flips rare near-ties).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+import golden_io
+import helpers
+import paper_2512_02175_b200 as gs
+from oracle import oracle
+from paper_2512_02175_b200 import analysis, engine
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.mark.parametrize("m", golden_io.meta()["ensembles"], ids=lambda m: m["name"])
+def test_reference_stream_ensembles_match_golden(m):
+    g, f, cfg, _ = helpers.config_for(m)
+    d = golden_io.load_npz_groups("ensembles.npz")[m["name"]]
+    r = gs.run_ensemble(g, f, cfg)
+    np.testing.assert_array_equal(r.edges, d["edges"])
+    np.testing.assert_array_equal(r.crossings, d["crossings"])
+    np.testing.assert_array_equal(r.crossing_events, d["crossing_events"])
+    np.testing.assert_array_equal(r.stats.m_histogram, d["m_histogram"])
+    assert [r.stats.truncation_count, r.stats.crossings_total, r.stats.crossing_events] == \
+        d["stats"].tolist()
+    assert r.stats.gamma == m["gamma"]
+    helpers.assert_positions(r.positions, d["positions"])
+
+
+@pytest.mark.parametrize("m", golden_io.meta()["trials"], ids=lambda m: m["name"])
+def test_reference_stream_trials_match_golden(m):
+    g, f = cases.build(m["case"], gs)
+    d = golden_io.load_npz_groups("trials.npz")[m["name"]]
+    tr = gs.vertex_crossing_trials(g, f, m["dt"], m["n"], m["seed"], vertex=m["vertex"],
+                                   max_splits=m["cap"], rng="reference")
+    np.testing.assert_array_equal(tr.M, d["M"])
+    np.testing.assert_array_equal(tr.exit_edges, d["exit_edges"])
+    np.testing.assert_array_equal(tr.truncated, d["truncated"])
+    helpers.assert_positions(tr.exit_positions, d["exit_positions"])
+    assert tr.gamma == m["gamma"]
+
+
+def _step_rows(case):
+    d = golden_io.load_npz_groups("steps.npz")[case]
+    # uint64 columns travel as int64 bit patterns (the kernels read uint64)
+    t = {k: torch.as_tensor(v.view(np.int64) if v.dtype == np.uint64 else v).to(DEV)
+         for k, v in d.items()}
+    return d, t
+
+
+@pytest.mark.parametrize("case", list(cases.CASES))
+def test_reference_stream_single_steps_match_golden(case):
+    g, f = cases.build(case, gs)
+    d, t = _step_rows(case)
+    # rows differ in dt / cap / reflect: group them
+    for dt_cap_refl in sorted(set(zip(d["dt"].tolist(), d["cap"].tolist(), d["refl"].tolist()))):
+        dt, cap, refl = dt_cap_refl
+        sel = np.flatnonzero((d["dt"] == dt) & (d["cap"] == cap) & (d["refl"] == refl))
+        s = torch.as_tensor(sel, device=DEV)
+        e, x, M, tr, k = engine.step_batch(g, f, t["edge"][s], t["x"][s], dt, t["seed"][s],
+                                           t["pid"][s], t["k"][s], cap, refl)
+        np.testing.assert_array_equal(e.cpu().numpy(), d["o_edge"][sel])
+        np.testing.assert_array_equal(M.cpu().numpy(), d["o_M"][sel])
+        np.testing.assert_array_equal(tr.cpu().numpy(), d["o_trunc"][sel])
+        np.testing.assert_array_equal(k.cpu().numpy().view(np.uint64), d["o_k"][sel])
+        xr = d["o_x"][sel]
+        xg = x.cpu().numpy()
+        assert np.all((xg == xr) | (np.abs(xg - xr) <= 1e-12 * np.abs(xr) + 1e-14))
+
+
+def test_em_step_api_matches_golden_rows():
+    for case in ("star5_linear", "random_general"):
+        g, f = cases.build(case, gs)
+        d = golden_io.load_npz_groups("steps.npz")[case]
+        for i in range(0, 40, 7):
+            st = gs.ParticleState(edge=int(d["edge"][i]), x=float(d["x"][i]))
+            rs = gs.RngStream(int(d["seed"][i]), int(d["pid"][i]), int(d["k"][i]))
+            if g.is_star:
+                o = gs.em_step_star(g, f, st, float(d["dt"][i]), rs, int(d["cap"][i]),
+                                    float(d["refl"][i]))
+            else:
+                o = gs.em_step_general(g, f, st, float(d["dt"][i]), rs, int(d["cap"][i]))
+            assert o.state.edge == d["o_edge"][i] and o.crossings_this_step == d["o_M"][i]
+            assert o.truncated == bool(d["o_trunc"][i]) and rs.counter == int(d["o_k"][i])
+            assert abs(o.state.x - d["o_x"][i]) <= 1e-12 * abs(d["o_x"][i]) + 1e-14
+
+
+def _oracle_run(g, f, seed, n, steps, dt, init, cap=100, refl=0.0):
+    return oracle.ensemble(oracle.OracleGraph(g, f), seed, n, steps, dt, init, cap, refl)
+
+
+@pytest.mark.parametrize("case,n,steps,dt,init", [
+    ("star3_bm", 10_000, 1000, 1e-3, ("at", 0)),            # C1 exactly
+    ("star5_quad", 20_000, 300, 1e-3, ("uniform", 0.4)),
+    ("hub64", 20_000, 300, 1e-3, ("uniform", 2.0)),
+    ("random_general", 20_000, 300, 2e-3, ("uniform", 1.0)),
+    ("vascular_small", 20_000, 200, 1e-3, ("uniform", 2.0)),
+])
+def test_reference_stream_vs_oracle_larger(case, n, steps, dt, init):
+    g, f = helpers.graph_for(case)
+    cfg = gs.SimulationConfig(dt=dt, n_steps=steps, n_particles=n, seed=20251202,
+                              initial=helpers.initial_for(init), rng="reference")
+    r = gs.run_ensemble(g, f, cfg)
+    o = _oracle_run(g, f, 20251202, n, steps, dt, helpers.oracle_init(init, g))
+    np.testing.assert_array_equal(r.edges, o["edges"])
+    np.testing.assert_array_equal(r.crossings, o["crossings"])
+    np.testing.assert_array_equal(r.crossing_events, o["crossing_events"])
+    np.testing.assert_array_equal(r.stats.m_histogram, o["m_histogram"])
+    helpers.assert_positions(r.positions, o["positions"])
+
+
+def _inject_tensors(seed, n, K, pid0=0):
+    raw, nrm = oracle.fill_draws(seed, n, K, pid0=pid0)
+    return torch.as_tensor(raw.view(np.int64)).to(DEV), torch.as_tensor(nrm).to(DEV)
+
+
+def test_inject_f64_equals_reference_stream():
+    g, f = cases.build("star4_mixed", gs)
+    cfg = gs.SimulationConfig(dt=1e-2, n_steps=100, n_particles=3000, seed=77, rng="reference",
+                              max_splits_per_step=5, initial=gs.PerEdgeUniform(0.2))
+    ref = engine.ensemble_device(g, f, cfg)
+    inj = engine.ensemble_device(g, f, cfg, inject=_inject_tensors(77, 3000, 1200),
+                                 precision="f64")
+    assert int(inj["totals"][3]) == 0
+    for k in ("edge", "x", "crossings", "events", "truncs", "m_hist"):
+        assert torch.equal(ref[k], inj[k]), k
+
+
+def test_inject_f32_single_steps_north_star_contract():
+    """Per-step FP32 parity restarted from reference states (SURVEY §7 hard part 1)."""
+    n_rows = n_tie = 0
+    for case in cases.CASES:
+        g, f = cases.build(case, gs)
+        d, t = _step_rows(case)
+        sig = f.packed()[5]
+        for dt, cap, refl in sorted(set(zip(d["dt"].tolist(), d["cap"].tolist(),
+                                            d["refl"].tolist()))):
+            sel = np.flatnonzero((d["dt"] == dt) & (d["cap"] == cap) & (d["refl"] == refl))
+            raw, nrm = oracle.fill_draws_rows(d["seed"][sel], d["pid"][sel], d["k"][sel],
+                                              2 * cap + 2)
+            inj = (torch.as_tensor(raw.view(np.int64)).to(DEV), torch.as_tensor(nrm).to(DEV))
+            s = torch.as_tensor(sel, device=DEV)
+            e, x, M, tr, k = engine.step_batch(g, f, t["edge"][s], t["x"][s], dt, None, None,
+                                               t["k"][s], cap, refl, inject=inj, precision="f32")
+            e, x, M = e.cpu().numpy(), x.cpu().numpy(), M.cpu().numpy()
+            ok_int = (e == d["o_edge"][sel]) & (M == d["o_M"][sel])
+            scale = np.maximum(np.abs(d["x"][sel]), sig[d["edge"][sel]] * np.sqrt(dt))
+            ok_x = np.abs(x - d["o_x"][sel]) <= 1e-5 * np.maximum(scale, np.abs(d["o_x"][sel]))
+            n_rows += sel.size
+            n_tie += int((~(ok_int & ok_x)).sum())
+    # FP32 vs FP64 can only disagree on decisions within FP32 rounding of a
+    # threshold; over 4800 random steps we allow at most 0.5% such rows.
+    assert n_tie <= 0.005 * n_rows, (n_tie, n_rows)
+
+
+def test_inject_f32_full_trajectories_c1():
+    """C1 (3-edge Brownian star, 1e4 x 1e3) in FP32 with the reference's draws."""
+    g, f = cases.build("star3_bm", gs)
+    n, steps = 10_000, 1000
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=steps, n_particles=n, seed=20251202)
+    out = engine.ensemble_device(g, f, cfg, inject=_inject_tensors(20251202, n, 1400),
+                                 precision="f32")
+    assert int(out["totals"][3]) == 0
+    o = _oracle_run(g, f, 20251202, n, steps, 1e-3, (0, 0, 0.0, 0.0))
+    e = out["edge"].cpu().numpy()
+    c = out["crossings"].cpu().numpy()
+    x = out["x"].cpu().numpy()
+    same = (e == o["edges"]) & (c == o["crossings"])
+    close = np.abs(x - o["positions"]) <= 1e-5 * np.maximum(np.abs(o["positions"]),
+                                                            np.sqrt(1e-3))
+    print(f"FP32 trajectories: exact edge+crossings {same.mean():.5f}, "
+          f"positions within 1e-5 {close.mean():.5f}")
+    assert same.mean() >= 0.999
+    assert (same & close).mean() >= 0.99
+
+
+def test_histogram_kernel_matches_oracle():
+    rng = np.random.default_rng(3)
+    g, _ = cases.build("hub8", gs)
+    grid = gs.EdgeGrid.uniform(g, 7)
+    n = 200_000
+    e = rng.integers(0, 8, n)
+    x = rng.uniform(-0.1, 1.1, n) * grid.lengths[e]
+    x[:100] = 0.0
+    x[100:200] = grid.lengths[e[100:200]]
+    x[200:300] = (rng.integers(0, 7, 100)) * grid.dx[e[200:300]]  # exact bin edges
+    h = analysis.histogram_accumulate(e, x, grid)
+    np.testing.assert_array_equal(h.counts, oracle.histogram(e, x, grid.offsets, grid.counts,
+                                                             grid.dx))
+    assert h.total == n
+    big = gs.EdgeGrid.uniform(g, 5000)  # > smem: global-atomics path
+    hb = analysis.histogram_accumulate(e, x, big)
+    np.testing.assert_array_equal(hb.counts, oracle.histogram(e, x, big.offsets, big.counts,
+                                                              big.dx))
+
+
+def test_golden_histogram_star3():
+    st = golden_io.meta()["stats"]["hist_star3"]
+    d = golden_io.load_npz_groups("ensembles.npz")["c1_star3_bm"]
+    g, _ = cases.build("star3_bm", gs)
+    grid = gs.EdgeGrid.uniform(g, st["cells"], lengths=st["lengths"])
+    h = analysis.histogram_accumulate(d["edges"], d["positions"], grid)
+    np.testing.assert_array_equal(h.counts, st["counts"])
+
+
+@pytest.mark.parametrize("rng", ["reference", "native"])
+def test_fused_histogram_equals_histogram_of_outputs(rng):
+    g, f = cases.build("hub64", gs)
+    grid = gs.EdgeGrid.uniform(g, 8)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=200, n_particles=50_000, seed=5,
+                              initial=gs.PerEdgeUniform(2.0), rng=rng)
+    r = gs.run_ensemble(g, f, cfg)
+    h, stats = analysis.run_ensemble_histogram(g, f, cfg, grid)
+    np.testing.assert_array_equal(h.counts, oracle.histogram(r.edges, r.positions, grid.offsets,
+                                                             grid.counts, grid.dx))
+    np.testing.assert_array_equal(stats.m_histogram, r.stats.m_histogram)
+
+
+def test_sharded_reference_run_equals_single_run():
+    g, f = cases.build("hub8", gs)
+    cfg = gs.SimulationConfig(dt=1e-2, n_steps=100, n_particles=10_001, seed=9,
+                              initial=gs.PerEdgeUniform(2.0), rng="reference")
+    full = engine.ensemble_device(g, f, cfg)
+    parts = [engine.ensemble_device(g, f, cfg, pid_offset=o, n_particles=c)
+             for o, c in ((0, 4000), (4000, 6001))]
+    for k in ("edge", "x", "crossings"):
+        assert torch.equal(full[k], torch.cat([p[k] for p in parts])), k
+    assert torch.equal(full["m_hist"], parts[0]["m_hist"] + parts[1]["m_hist"])
