@@ -1,0 +1,497 @@
+#!/usr/bin/env python
+"""Benchmark: particle-steps/s of the timestep-splitting EM simulator on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload star3|hub64|star5_trials|vascular] [--no-extras]
+
+One bench "step" = one pass of the hot path over the workload's batch: one
+``run_ensemble``-equivalent launch (all particles x all macro steps, fused
+M-histogram / occupancy / snapshot-histogram estimators) plus, for N > 1, the
+NCCL all-reduce that merges the estimators.  Default workload = C1 throughput
+variant: 3-edge Brownian star, 1.6e7 particles per GPU x
+1000 steps, dt = 1e-3 -- the configuration the north-star target
+(>= 1e11 psteps/s per B200) is quoted on.  Particles shard by global id
+(weak scaling); no data-path collective.
+
+Rank 0 prints ONE JSON line.  ``value`` is device-timed (CUDA events, max
+over ranks) with inputs resident; ``e2e`` goes through the public API
+(``run_ensemble``: graph upload + kernel + D2H of the reference-dtype result
+arrays) with host buffers.  ``--impl reference`` times the reference
+algorithm on the host CPU (the C restatement in oracle/, all host threads).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "particle-steps/sec (1/2/4/8 B200) and fraction of FP32 roofline vs CPU ref"
+UNIT = "psteps/s"
+
+
+# ----------------------------------------------------------------------------
+# workloads
+class Workload:
+    name = ""
+    desc = ""
+    unit = UNIT
+
+    def __init__(self, rank=0, world=1):
+        self.rank, self.world = rank, world
+
+
+class Ensemble(Workload):
+    def __init__(self, name, desc, build, n_per_gpu, n_steps, dt, initial, grid_fn, rank=0,
+                 world=1):
+        super().__init__(rank, world)
+        import paper_2512_02175_b200 as gs
+
+        self.name, self.desc = name, desc
+        self.g, self.f = build()
+        self.n, self.n_steps, self.dt = n_per_gpu, n_steps, dt
+        self.initial = initial(self.g)
+        self.grid = grid_fn(self.g)
+        self.cfg = gs.SimulationConfig(dt=dt, n_steps=n_steps, n_particles=n_per_gpu * world,
+                                       seed=20251202, initial=self.initial, rng="native")
+        self.units_per_step = n_per_gpu * n_steps  # per GPU
+
+    def config(self):
+        return {"workload": self.desc, "n_particles_per_gpu": self.n, "n_steps": self.n_steps,
+                "dt": self.dt, "graph_edges": self.g.n_edges, "rng": "native (FP32, Philox4x32-10)"}
+
+    def launch(self, stream):
+        from paper_2512_02175_b200 import engine
+
+        return engine.ensemble_device(self.g, self.f, self.cfg, pid_offset=self.rank * self.n,
+                                      n_particles=self.n, outputs=("edge_counts",),
+                                      grid=self.grid, stream=stream)
+
+    def reduce_tensor(self, res):
+        import torch
+
+        return torch.cat([res["m_hist"], res["totals"], res["edge_counts"], res["hist"]])
+
+    def crossings(self, res):
+        return int(res["totals"][0])
+
+    def e2e_call(self):
+        import paper_2512_02175_b200 as gs
+
+        self.g._device.clear()  # inputs travel every step: graph + field upload
+        r = gs.run_ensemble(self.g, self.f, self.cfg_single())
+        d2h = sum(a.nbytes for a in (r.edges, r.positions, r.crossings, r.crossing_events))
+        return d2h + r.stats.m_histogram.nbytes
+
+    def cfg_single(self):
+        import dataclasses
+
+        return dataclasses.replace(self.cfg, n_particles=self.n)
+
+    def cpu_sample(self, scale):
+        """(oracle callable, units) for a bounded CPU sample."""
+        from oracle import oracle
+
+        og = oracle.OracleGraph(self.g, self.f)
+        from paper_2512_02175_b200.engine import _resolve_initial
+
+        init = _resolve_initial(self.g, self.initial)
+        n = max(4096, int(scale))
+
+        def run(threads):
+            oracle.ensemble(og, 20251202, n, self.n_steps, self.dt, init, 100, 0.0,
+                            threads=threads)
+
+        return run, n * self.n_steps, f"{n} particles x {self.n_steps} steps"
+
+
+class Trials(Workload):
+    unit = "trials/s"
+
+    def __init__(self, rank=0, world=1, n_per_gpu=250_000_000, dt=1e-3):
+        super().__init__(rank, world)
+        from paper_2512_02175_b200 import workloads
+
+        self.name = "star5_trials"
+        self.desc = ("C3: paper §4.1 5-edge star, ConstantDrift(-10 i), vertex trials at "
+                     f"dt={dt} (fused exit counts + M histogram)")
+        self.g, self.f = workloads.star5("linear")
+        self.n, self.dt = n_per_gpu, dt
+        self.units_per_step = n_per_gpu
+
+    def config(self):
+        return {"workload": self.desc, "n_trials_per_gpu": self.n, "dt": self.dt}
+
+    def launch(self, stream):
+        from paper_2512_02175_b200 import engine
+
+        return engine.trials_device(self.g, self.f, self.dt, self.n, 11, per_trial=False,
+                                    trial_offset=self.rank * self.n, stream=stream)
+
+    def reduce_tensor(self, res):
+        import torch
+
+        return torch.cat([res["exit_counts"], res["m_hist"], res["totals"]])
+
+    def crossings(self, res):
+        return int(res["totals"][0])
+
+
+def make_workload(name, rank, world):
+    import paper_2512_02175_b200 as gs
+    from paper_2512_02175_b200 import workloads
+
+    if name == "star3":
+        return Ensemble(
+            "star3", "C1-throughput: 3-edge star, Brownian (mu=0, sigma=1), AtVertex(0), "
+            "dt=1e-3, 1000 steps, 1.6e7 particles/GPU; fused 3x16-cell histogram + occupancy",
+            workloads.star3, 16_000_000, 1000, 1e-3, lambda g: gs.AtVertex(0),
+            lambda g: gs.EdgeGrid.uniform(g, 16, lengths=[3.0] * 3), rank, world)
+    if name == "hub64":
+        return Ensemble(
+            "hub64", "C2: 64-edge hub (lengths U[0.5,2]), LinearDrift(-k_i) quadratic potential, "
+            "PerEdgeUniform(2.0), dt=1e-3, 1000 steps, 1e8 particles/GPU; fused 64x8 histogram",
+            workloads.hub64, 100_000_000, 1000, 1e-3, lambda g: gs.PerEdgeUniform(2.0),
+            lambda g: gs.EdgeGrid.uniform(g, 8), rank, world)
+    if name == "vascular":
+        return Ensemble(
+            "vascular", "C4/C5: synthetic vascular network (~1.02e5 edges, kNN-MST + 2% loops), "
+            "drift from_flux, PerEdgeUniform(max l), dt=1e-3, 100 steps, 1e8 particles/GPU; "
+            "fused 8-cell/edge histogram",
+            _vascular_cached, 100_000_000, 100, 1e-3,
+            lambda g: gs.PerEdgeUniform(float(g.edge_length.max())),
+            lambda g: gs.EdgeGrid.uniform(g, 8), rank, world)
+    if name == "star5_trials":
+        return Trials(rank, world)
+    raise SystemExit(f"unknown workload {name}")
+
+
+_VASC = None
+
+
+def _vascular_cached():
+    global _VASC
+    if _VASC is None:
+        from paper_2512_02175_b200 import workloads
+
+        _VASC = workloads.vascular()
+    return _VASC
+
+
+# ----------------------------------------------------------------------------
+# measurement helpers
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def flush_l2(buf):
+    buf.fill_(1)  # 256 MiB write > 126 MB L2
+
+
+def lane_ops_per_pstep(crossings_per_pstep):
+    """SURVEY.md §8(d) / BASELINE.md §3: W = 40 + 70 c lane-ops per pstep."""
+    return 40.0 + 70.0 * crossings_per_pstep
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(workload)
+    except OSError:
+        return None
+
+
+# ----------------------------------------------------------------------------
+def cpu_baseline(wl, seconds=12.0):
+    """Oracle (C port of the reference algorithm, OpenMP over particle chunks,
+    all host threads) on a bounded sample of the same workload."""
+    from oracle import oracle
+
+    threads = os.cpu_count() or 1
+    if isinstance(wl, Trials):
+        og = oracle.OracleGraph(wl.g, wl.f)
+        n_cal = 200_000
+        t0 = time.perf_counter()
+        oracle.vertex_trials(og, 11, n_cal, wl.dt, threads=threads)
+        rate = n_cal / max(time.perf_counter() - t0, 1e-6)
+        n = int(min(max(rate * seconds, n_cal), 2e9))
+        t0 = time.perf_counter()
+        oracle.vertex_trials(og, 11, n, wl.dt, threads=threads)
+        dt = time.perf_counter() - t0
+        return {"value": n / dt, "unit": wl.unit, "cores": threads, "kind": "port",
+                "sample": f"{n} trials (oracle/gsde_oracle.c, {threads} threads)"}
+    run, units, desc = wl.cpu_sample(20_000)
+    t0 = time.perf_counter()
+    run(threads)
+    rate = units / max(time.perf_counter() - t0, 1e-6)
+    run, units, desc = wl.cpu_sample(20_000 * max(1.0, rate * seconds / units))
+    t0 = time.perf_counter()
+    run(threads)
+    dt = time.perf_counter() - t0
+    return {"value": units / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{desc} (oracle/gsde_oracle.c, {threads} threads)"}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    wl = make_workload(args.workload, 0, 1)
+    base = cpu_baseline(wl, seconds=2.0)  # calibrates a ~2 s step
+    rate = base["value"]
+    from oracle import oracle  # noqa: F401
+
+    threads = os.cpu_count() or 1
+    if isinstance(wl, Trials):
+        og = oracle.OracleGraph(wl.g, wl.f)
+        n = int(rate * 2.0)
+        step = lambda: oracle.vertex_trials(og, 11, n, wl.dt, threads=threads)
+        units, sample = n, f"{n} trials per step"
+    else:
+        run, units, sample = wl.cpu_sample(max(4096, rate * 2.0 / wl.n_steps))
+        step = lambda: run(threads)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = units * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": dict(wl.config(), sample=sample),
+        "cpu_baseline": {"value": value, "unit": wl.unit, "cores": threads, "kind": "port",
+                         "sample": f"{sample} (oracle/gsde_oracle.c: C restatement of the "
+                                   "reference numba kernels; reference is Python)"},
+        "e2e": {"value": value, "unit": wl.unit, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_workload(wl, steps, warmup, dist, torch, dev, flush_buf, clocks_index=None):
+    """Returns (elapsed_s max over ranks, kernel_s, res, launches)."""
+    from paper_2512_02175_b200 import _native
+
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        res = wl.launch(stream.cuda_stream)
+        if dist is not None:
+            dist.all_reduce(wl.reduce_tensor(res))
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = _native.launch_count()
+    total = 0.0
+    kern = 0.0
+    sampler = ClockSampler(clocks_index) if clocks_index is not None else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        for _ in range(steps):
+            flush_l2(flush_buf)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = wl.launch(stream.cuda_stream)
+            e1.record(stream)
+            if dist is not None:
+                dist.all_reduce(wl.reduce_tensor(res))
+            e2.record(stream)
+            e2.synchronize()
+            total += e0.elapsed_time(e2) / 1e3
+            kern += e0.elapsed_time(e1) / 1e3
+    finally:
+        if sampler:
+            sampler.__exit__()
+    torch.cuda.synchronize(dev)
+    launches = _native.launch_count() - l0
+    if dist is not None:
+        dist.barrier()
+        t = torch.tensor([total, kern], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total, kern = float(t[0]), float(t[1])
+    return total, kern, res, launches, (sampler.summary() if sampler else None)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="star3",
+                    choices=["star3", "hub64", "star5_trials", "vascular"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "RANK" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = local
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist = tdist
+    import paper_2512_02175_b200 as gs  # noqa: F401
+    from paper_2512_02175_b200 import _native
+
+    _native.lib()
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    wl = make_workload(args.workload, rank, world)
+    total, kern, res, launches, clocks = time_workload(
+        wl, args.steps, args.warmup, dist, torch, dev, flush_buf,
+        clocks_index=torch.cuda.current_device() if rank == 0 else None)
+    units = wl.units_per_step * world * args.steps
+    value = units / total
+    crossings = wl.crossings(res)
+    c_per = crossings / wl.units_per_step
+
+    peaks = measured_peaks()
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_ops = sm_count * 128 * f_max * 1e6
+    w_ops = lane_ops_per_pstep(c_per)
+    kern_rate = wl.units_per_step * args.steps / kern  # per GPU, kernel only
+    achieved = kern_rate * w_ops
+
+    line = None
+    if rank == 0:
+        # e2e through the public API with host buffers (graph upload + D2H)
+        e2e = None
+        if hasattr(wl, "e2e_call"):
+            wl.e2e_call()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            nbytes = 0
+            for _ in range(max(1, min(args.steps, 3))):
+                nbytes = wl.e2e_call()
+            el = (time.perf_counter() - t0) / max(1, min(args.steps, 3))
+            dg = _native.device_graph(wl.g, wl.f, dev)
+            e2e = {"value": wl.units_per_step / el, "unit": wl.unit,
+                   "h2d_bytes_per_step": int(dg.device_bytes),
+                   "d2h_bytes_per_step": int(nbytes),
+                   "path": "paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble), "
+                           "reference-dtype result arrays to host"}
+        line = {
+            "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded graph generators, random streams; no external data)",
+            "config": dict(wl.config(), parallelism=f"particle-sharded x{world}",
+                           l2="flushed between steps (256 MiB write)"),
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "roofline": {
+                "bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
+                "unit": "Tlane-op/s", "frac": achieved / peak_ops,
+                "traffic": load_traffic(wl.name),
+                "work_model": f"W = 40 + 70 c lane-ops/pstep, c = {c_per:.4f} crossings/pstep "
+                              f"(BASELINE.md §3); peak = {sm_count} SM x 128 lanes x "
+                              f"{f_max:.0f} MHz ({'MEASURED_PEAKS.json' if peaks else 'nominal'})",
+                "kernel_ms_per_step": kern / args.steps * 1e3,
+            },
+            "crossings_per_pstep": c_per,
+        }
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(wl)
+        if not args.no_extras and world == 1:
+            extras = {}
+            for name in ("hub64", "star5_trials", "vascular"):
+                if name == args.workload:
+                    continue
+                w2 = make_workload(name, 0, 1)
+                t2, k2, r2, _, _ = time_workload(w2, 2, 1, None, torch, dev, flush_buf)
+                c2 = w2.crossings(r2) / w2.units_per_step
+                rate2 = w2.units_per_step * 2 / t2
+                extras[name] = {"value": rate2, "unit": w2.unit, "config": w2.config(),
+                                "crossings_per_unit": c2,
+                                "roofline_frac": rate2 * lane_ops_per_pstep(c2) / peak_ops}
+            line["workloads"] = extras
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
