@@ -26,21 +26,32 @@ struct Block {
   uint32_t x, y, z, w;
 };
 
-// 10 rounds; each round: two 32x32->64 products (one IMAD.WIDE each on the
-// device), two 3-input xors (LOP3), key bump (uniform across the warp).
+// 32x32 -> 64-bit product split into (hi, lo).  On the device this is one
+// IMAD.WIDE.U32 (mul.wide.u32); a C++ 64-bit multiply makes ptxas add a
+// redundant high-word add per round.
+GSDE_HD void mul_hilo(uint32_t a, uint32_t b, uint32_t &hi, uint32_t &lo) {
+#if defined(__CUDA_ARCH__)
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
+#else
+  const uint64_t p = (uint64_t)a * b;
+  hi = (uint32_t)(p >> 32);
+  lo = (uint32_t)p;
+#endif
+}
+
+// 10 rounds; each round: two 32x32->64 products (IMAD.WIDE), two 3-input
+// xors (LOP3), key bump (uniform across the warp).
 GSDE_HD Block philox4x32_10(Block c, uint32_t k0, uint32_t k1) {
 #if defined(__CUDA_ARCH__)
 #pragma unroll
 #endif
   for (int r = 0; r < 10; ++r) {
-    const uint64_t p0 = (uint64_t)kPhiloxM0 * c.x;
-    const uint64_t p1 = (uint64_t)kPhiloxM1 * c.z;
-    Block n;
-    n.x = (uint32_t)(p1 >> 32) ^ c.y ^ k0;
-    n.y = (uint32_t)p1;
-    n.z = (uint32_t)(p0 >> 32) ^ c.w ^ k1;
-    n.w = (uint32_t)p0;
-    c = n;
+    uint32_t hi0, lo0, hi1, lo1;
+    mul_hilo(c.x, kPhiloxM0, hi0, lo0);
+    mul_hilo(c.z, kPhiloxM1, hi1, lo1);
+    c = Block{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
     k0 += kPhiloxW0;
     k1 += kPhiloxW1;
   }

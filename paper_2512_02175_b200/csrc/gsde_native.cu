@@ -5,21 +5,27 @@
 //    assigned by grid stride; all per-particle state lives in registers for
 //    the whole run;
 //  * flattened state machine: every loop trip performs exactly one proposal
-//    per lane -- either a free Euler-Maruyama step or one vertex iteration --
-//    so split/excursion loops never serialise a warp (kernels.py:198-220 and
-//    :257-288 become extra trips of the same loop body);
+//    per lane -- a free Euler-Maruyama step or one vertex iteration -- so the
+//    split / excursion loops of kernels.py:198-220 and :257-288 become extra
+//    trips of the same loop body and never serialise a warp;
+//  * common path is branch-free: a lane strictly inside an edge always starts
+//    a fresh macro step (dtr == dt), so its proposal is 3 FFMAs with cached
+//    per-edge constants and the accept test is 2-4 compares.  Everything else
+//    (vertex iterations, splits, reflections, statistics) is one divergent
+//    "rare" region per trip, followed by an explicit warp reconvergence;
 //  * RNG: one Philox4x32-10 block per TWO trips, counter (trip pair, domain,
 //    particle id) under the seed: words 0,1 -> Box-Muller -> the trips'
 //    Gaussians, words 2,3 -> the trips' 32-bit exit-slot uniforms.  Every
-//    trip consumes the same amount, so lanes stay phase-aligned and the block
-//    is generated warp-convergently;
-//  * exit slot: per-vertex alias table, one column record (16 B) per pick;
-//  * star graphs / small graphs: edge records + alias columns staged in
-//    shared memory; large networks read them through L2 (__ldg);
-//  * estimators fused: M histogram in lane-private shared counters
-//    (M < kPriv) + shared atomics, final-edge occupancy and snapshot histogram
-//    in the epilogue, totals warp-reduced.
+//    trip consumes the same amount, so all lanes generate blocks in lockstep;
+//  * exit slot: per-vertex alias table, one 16 B column record per pick;
+//  * star / small graphs: edge records and alias columns staged in shared
+//    memory; large networks read them through L2 (__ldg);
+//  * estimators fused: M histogram in lane-private shared counters (M < 8)
+//    + shared atomics; totals in shared memory; occupancy and snapshot
+//    histogram in the particle epilogue.
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "gsde_epilogue.cuh"
 
@@ -27,12 +33,14 @@ namespace gsde {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPriv = 8;  // lane-private M-histogram bins
+constexpr int kMinBlocks = 4;  // caps registers at 64 -> 32 warps / SM
+constexpr int kPriv = 8;       // lane-private M-histogram bins
 constexpr uint32_t kDomainEnsemble = 0u;
 constexpr uint32_t kDomainTrials = 1u;
 constexpr uint32_t kDomainPlace = 0xFFFFFFFFu;
 
 struct NatParams {
+  uint32_t rk[20];    // Philox round keys of the seed (constant-bank operands)
   uint64_t seed;
   int64_t n;          // particles / trials in this call
   int64_t id_offset;  // global id of item 0
@@ -46,21 +54,95 @@ struct NatParams {
   double init_xmax;
   int32_t start_edge; // trials (general)
   float start_x;
-  int32_t smem_graph;
 };
+
+__device__ __forceinline__ float fast_sqrt(float v) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+__device__ __forceinline__ float fast_lg2(float v) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
 
 // Box-Muller on two 32-bit words: u1 in (0, 1] with 2^-33 resolution near 0
 // (|z| <= 6.8), angle uniform on [-pi, pi).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = fmaf((float)a, 0x1p-32f, 0x1p-33f);
-  const float r = sqrtf(fmaxf(-2.0f * __logf(u1), 0.0f));
+  const float r = fast_sqrt(fmaxf(fast_lg2(u1) * -1.3862943611198906f, 0.0f));  // -2 ln u1
   float s, c;
-  __sincosf((float)(int32_t)b * 0x1p-31f * 3.14159265358979f, &s, &c);
+  __sincosf((float)(int32_t)b * 7.3145904512e-10f, &s, &c);  // pi * 2^-31
   z0 = r * c;
   z1 = r * s;
 }
 
-__device__ __forceinline__ float drift_tab(const NativeGraph &G, int e, float x) {
+// kernels.py:88-131 in FP32 with approximate division / square root.
+__device__ __forceinline__ float solve_fast(float a, float b, float c) {
+  if (c < 0.0f) return 0.0f;
+  if (c == 0.0f) {
+    if (b <= 0.0f) return 0.0f;
+    if (a >= 0.0f) return -1.0f;
+    return fminf(__fdividef(-b, a), 1.0f);
+  }
+  if (a == 0.0f) {
+    if (b >= 0.0f) return -1.0f;
+    return fminf(__fdividef(-c, b), 1.0f);
+  }
+  const float disc = fmaxf(b * b - 4.0f * a * c, 0.0f);
+  const float sq = fast_sqrt(disc);
+  const float q = b >= 0.0f ? -0.5f * (b + sq) : -0.5f * (b - sq);
+  float s = -1.0f;
+  const float r1 = __fdividef(q, a);
+  if (r1 >= 0.0f) s = r1;
+  if (q != 0.0f) {
+    const float r2 = __fdividef(c, q);
+    if (r2 >= 0.0f && (s < 0.0f || r2 < s)) s = r2;
+  }
+  return s < 0.0f ? -1.0f : fminf(s, 1.0f);
+}
+
+// Philox4x32-10 with the key schedule precomputed in the kernel parameters:
+// per round 2 IMAD.WIDE + 2 LOP3 (the round key is a constant-bank operand).
+__device__ __forceinline__ Block native_block(const NatParams &p, uint32_t pair, uint32_t domain,
+                                              uint64_t id) {
+  Block c{pair, domain, (uint32_t)id, (uint32_t)(id >> 32)};
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mul_hilo(c.x, kPhiloxM0, hi0, lo0);
+    mul_hilo(c.z, kPhiloxM1, hi1, lo1);
+    c = Block{hi1 ^ c.y ^ p.rk[2 * r], lo1, hi0 ^ c.w ^ p.rk[2 * r + 1], lo0};
+  }
+  return c;
+}
+
+__device__ __forceinline__ size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+// Graph tables: shared-memory copies (SMEM) or global/L2 (read-only path).
+template <bool SMEM>
+struct Tables {
+  const float4 *edge;
+  const int4 *edgev;
+  const int4 *col;
+  __device__ __forceinline__ float4 E(int e) const { return SMEM ? edge[e] : __ldg(edge + e); }
+  __device__ __forceinline__ int4 V(int e) const { return SMEM ? edgev[e] : __ldg(edgev + e); }
+  __device__ __forceinline__ int4 C(int j) const { return SMEM ? col[j] : __ldg(col + j); }
+};
+
+// Alias pick with a 32-bit uniform: column = floor(u * deg), then the
+// column's threshold on the low word.  Returns edge | orient << 31.
+template <bool SMEM>
+__device__ __forceinline__ int alias_pick(const Tables<SMEM> &T, int off, int deg, uint32_t u) {
+  uint32_t hi, lo;
+  mul_hilo(u, (uint32_t)deg, hi, lo);
+  const int4 c = T.C(off + (int)hi);
+  return lo < (uint32_t)c.x ? c.y : c.z;
+}
+
+__device__ float drift_tab(const NativeGraph &G, int e, float x) {
   const int lo = G.tab_off[e], hi = G.tab_off[e + 1];
   if (x <= G.tab_x[lo]) return G.tab_mu[lo];
   if (x >= G.tab_x[hi - 1]) return G.tab_mu[hi - 1];
@@ -71,165 +153,196 @@ __device__ __forceinline__ float drift_tab(const NativeGraph &G, int e, float x)
   return G.tab_mu[j - 1] + t * (G.tab_mu[j] - G.tab_mu[j - 1]);
 }
 
-__device__ __forceinline__ float drift(const NativeGraph &G, const float4 &ep, int e, float x) {
-  if (G.has_tab && isnan(ep.z)) return drift_tab(G, e, x);
-  return fmaf(ep.z, x, ep.y);
-}
-
-// Alias pick with a 32-bit uniform: column = floor(u * deg), then the
-// column's threshold on the low word.  Returns edge | orient << 31.
-__device__ __forceinline__ int alias_pick(const int4 *cols, int off, int deg, uint32_t u) {
-  const uint64_t t = (uint64_t)u * (uint32_t)deg;
-  const int4 c = cols[off + (int)(t >> 32)];
-  return (uint32_t)t < (uint32_t)c.x ? c.y : c.z;
-}
-
-// Shared-memory layout: [priv: kPriv * kThreads ints][mh: cap+1 ints][pad]
-// [edges E float4][edgev E int4][cols S int4]  (graph part optional).
-struct Smem {
-  int *priv;
-  int *mh;
-  const float4 *edge;
-  const int4 *edgev;
-  const int4 *col;
+// Shared block state: lane-private M counters, M histogram, totals, staged graph.
+struct Shared {
+  int *priv;                 // [kPriv][kThreads]
+  int *mh;                   // [cap+1]
+  unsigned long long *tot;   // [4]
+  int *exit_priv;            // trials: [E][kThreads] or null
 };
 
-__device__ __forceinline__ size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+__device__ __forceinline__ size_t shared_head_bytes(int nb) {
+  return align16((size_t)(kPriv * kThreads + nb) * sizeof(int)) + 4 * sizeof(unsigned long long);
+}
 
-__device__ Smem smem_setup(const NativeGraph &G, int nb, int stage_graph, bool star) {
+template <bool STAR, bool SMEM>
+__device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, Shared &S,
+                                             Tables<SMEM> &T, bool exit_priv) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Smem S;
   S.priv = reinterpret_cast<int *>(smem);
   S.mh = S.priv + kPriv * kThreads;
-  size_t off = align16((size_t)(kPriv * kThreads + nb) * sizeof(int));
+  S.tot = reinterpret_cast<unsigned long long *>(
+      smem + align16((size_t)(kPriv * kThreads + nb) * sizeof(int)));
   for (int j = threadIdx.x; j < kPriv * kThreads + nb; j += blockDim.x) S.priv[j] = 0;
-  S.edge = G.edge;
-  S.edgev = G.edgev;
-  S.col = G.col;
-  if (stage_graph) {
+  if (threadIdx.x < 4) S.tot[threadIdx.x] = 0ull;
+  size_t off = shared_head_bytes(nb);
+  T.edge = G.edge;
+  T.edgev = G.edgev;
+  T.col = G.col;
+  if (SMEM) {
     float4 *se = reinterpret_cast<float4 *>(smem + off);
     off += (size_t)G.n_edges * sizeof(float4);
     int4 *sv = reinterpret_cast<int4 *>(smem + off);
-    if (!star) off += (size_t)G.n_edges * sizeof(int4);
+    if (!STAR) off += (size_t)G.n_edges * sizeof(int4);
     int4 *sc = reinterpret_cast<int4 *>(smem + off);
+    off += (size_t)G.n_slots * sizeof(int4);
     for (int j = threadIdx.x; j < G.n_edges; j += blockDim.x) {
       se[j] = G.edge[j];
-      if (!star) sv[j] = G.edgev[j];
+      if (!STAR) sv[j] = G.edgev[j];
     }
     for (int j = threadIdx.x; j < G.n_slots; j += blockDim.x) sc[j] = G.col[j];
-    S.edge = se;
-    S.edgev = sv;
-    S.col = sc;
+    T.edge = se;
+    T.edgev = sv;
+    T.col = sc;
+  }
+  S.exit_priv = nullptr;
+  if (exit_priv) {
+    S.exit_priv = reinterpret_cast<int *>(smem + off);
+    for (int j = threadIdx.x; j < G.n_edges * kThreads; j += blockDim.x) S.exit_priv[j] = 0;
   }
   __syncthreads();
-  return S;
 }
 
-__device__ __forceinline__ void mh_add(const Smem &S, int bin) {
+__device__ __forceinline__ void mh_add(const Shared &S, int bin) {
   if (bin < kPriv)
     S.priv[bin * kThreads + threadIdx.x] += 1;
   else
     atomicAdd(&S.mh[bin], 1);
 }
 
-__device__ void mh_flush(const Smem &S, int nb, int64_t *dst) {
+__device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int64_t *totals,
+                             int n_tot) {
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     int64_t v = S.mh[b];
     if (b < kPriv)
       for (int t = 0; t < kThreads; ++t) v += S.priv[b * kThreads + t];
-    if (v && dst) add_i64(&dst[b], v);
+    if (v && m_hist) add_i64(&m_hist[b], v);
   }
+  if (totals && threadIdx.x < n_tot && S.tot[threadIdx.x])
+    add_i64(&totals[threadIdx.x], (int64_t)S.tot[threadIdx.x]);
 }
 
 // Per-lane simulation state.
+template <bool STAR, bool SMEM>
 struct Lane {
-  int e;        // current edge
-  float x;      // position on e
-  float dtr;    // time left in the current macro step
-  float sq;     // sqrt(dtr)
-  int M;        // vertex resolutions in the current macro step
+  int e;           // current edge
+  float x;         // position on e
+  float dtr, sq;   // time left in the current macro step and its sqrt
+  int M;           // vertex resolutions in the current macro step
   bool trunc;
-  float4 ep;    // cached edge record of e
-  int4 ev;      // cached endpoint alias info of e (general graphs)
+  float mu_a, mu_b, sig, sig_sqdt;  // cached drift / diffusion of e
+  float len;       // edge length (star: mirror wall or +inf)
+  int4 ev;         // endpoint alias info of e (general graphs)
+  int steps_left;
+  int cross, events, truncs;
+
+  __device__ __forceinline__ void load_edge(const Tables<SMEM> &T, int e2, float sqdt,
+                                            float star_len) {
+    const float4 r = T.E(e2);
+    e = e2;
+    mu_a = r.y;
+    mu_b = r.z;
+    sig = r.w;
+    sig_sqdt = r.w * sqdt;
+    if (STAR) {
+      len = star_len;
+    } else {
+      len = r.x;
+      ev = T.V(e2);
+    }
+  }
+
+  template <bool TAB>
+  __device__ __forceinline__ float drift(const NativeGraph &G, float at) const {
+    if (TAB && isnan(mu_b)) return drift_tab(G, e, at);
+    return fmaf(mu_b, at, mu_a);
+  }
+
+  // macro step finished: statistics, reset for the next step
+  __device__ __forceinline__ void step_done(const Shared &S, int cap, float dt, float sqdt) {
+    if (M > 0) {
+      cross += M;
+      events += 1;
+      truncs += trunc ? 1 : 0;
+      mh_add(S, M > cap ? cap : M);
+    }
+    M = 0;
+    trunc = false;
+    dtr = dt;
+    sq = sqdt;
+  }
 };
 
-// One trip of the star-graph state machine (kernels.py:146-220 semantics).
-// Returns true when the macro step completed.
-__device__ __forceinline__ bool star_trip(Lane &L, const NativeGraph &G, const Smem &S,
-                                          const NatParams &p, float z, uint32_t u) {
-  const bool at_v = !(L.x > 0.0f);
-  float4 ep = L.ep;
-  int e = L.e;
-  float xb = L.x, w = z;
-  if (at_v) {  // sample the exit edge, one-sided excursion
-    e = alias_pick(S.col, 0, G.n_edges, u) & 0x7fffffff;
-    ep = S.edge[e];
-    xb = 0.0f;
-    w = fabsf(z);
-    L.M += 1;
-  }
-  const float mu = drift(G, ep, e, xb);
-  const float a = mu * L.dtr;
-  const float b = ep.w * L.sq * w;
-  float xn = xb + a + b;
-  const bool acc = at_v ? (xn >= 0.0f) : (xn > 0.0f);
-  L.e = e;
-  L.ep = ep;
-  if (acc) {
-    if (p.reflect > 0.0f && xn > p.reflect) xn = fmaxf(2.0f * p.reflect - xn, 0.0f);
-    L.x = xn;
-    return true;
-  }
-  L.x = 0.0f;
-  if (at_v) {  // failed excursion: consume its return time (Alg. 1)
-    const float alpha = (w * w * ep.w * ep.w) / (mu * mu * L.dtr);
-    L.dtr = (1.0f - alpha) * L.dtr;
-    if (L.dtr <= 0.0f) return true;
-    if (L.M >= p.cap) {
-      L.trunc = true;
+// Rare trip of a star graph (kernels.py:146-220 semantics).  Returns true when
+// the macro step completed.
+template <bool SMEM, bool TAB>
+__device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph &G,
+                                          const Tables<SMEM> &T, const NatParams &p,
+                                          float z, uint32_t u, float mu) {
+  if (L.x > 0.0f) {  // free step from the interior (dtr == dt)
+    const float xn = fmaf(L.sig_sqdt, z, fmaf(mu, p.dt, L.x));
+    if (xn > 0.0f) {  // beyond the mirror wall
+      L.x = fmaxf(2.0f * p.reflect - xn, 0.0f);
       return true;
     }
-  } else {  // free step overshot: split at the vertex
-    float s = solve_first_passage_s<float>(a, b, xb);
+    float s = solve_fast(mu * p.dt, L.sig_sqdt * z, L.x);
     if (s < 0.0f) s = 1.0f;
-    L.dtr = fmaxf((1.0f - s * s) * L.dtr, 0.0f);
+    L.dtr = fmaxf((1.0f - s * s) * p.dt, 0.0f);
+    L.sq = fast_sqrt(L.dtr);
+    L.x = 0.0f;
+    return false;
   }
-  L.sq = sqrtf(L.dtr);
+  // at the vertex: sample the exit edge, one-sided |W| excursion
+  L.M += 1;
+  L.load_edge(T, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
+  const float w = fabsf(z);
+  const float mu0 = L.template drift<TAB>(G, 0.0f);
+  const float xn = fmaf(L.sig * L.sq, w, mu0 * L.dtr);
+  if (xn >= 0.0f) {
+    L.x = (p.reflect > 0.0f && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
+    return true;
+  }
+  const float alpha = __fdividef(w * w * L.sig * L.sig, mu0 * mu0 * L.dtr);
+  L.dtr = (1.0f - alpha) * L.dtr;
+  L.x = 0.0f;
+  if (L.dtr <= 0.0f) return true;
+  if (L.M >= p.cap) {
+    L.trunc = true;
+    return true;
+  }
+  L.sq = fast_sqrt(L.dtr);
   return false;
 }
 
-// One trip of the general-graph state machine (kernels.py:223-288 semantics).
-__device__ __forceinline__ bool general_trip(Lane &L, const NativeGraph &G, const Smem &S,
-                                             const NatParams &p, float z, uint32_t u) {
+// Rare trip of a general graph (kernels.py:223-288 semantics).
+template <bool SMEM, bool TAB>
+__device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeGraph &G,
+                                             const Tables<SMEM> &T, const NatParams &p,
+                                             float z, uint32_t u) {
   const bool at_init = !(L.x > 0.0f);
-  const bool at_term = !(L.x < L.ep.x);
+  const bool at_term = !(L.x < L.len);  // (x == len exactly: the far vertex)
   if (at_init || at_term) {  // resample the exit slot at the hit vertex
-    const int off = at_init ? L.ev.x : L.ev.z;
-    const int deg = at_init ? L.ev.y : L.ev.w;
-    const int s = alias_pick(S.col, off, deg, u);
-    L.e = s & 0x7fffffff;
-    L.ep = S.edge[L.e];
-    L.ev = S.edgev[L.e];
-    L.x = s < 0 ? L.ep.x : 0.0f;
+    const int s = alias_pick(T, at_init ? L.ev.x : L.ev.z, at_init ? L.ev.y : L.ev.w, u);
+    L.load_edge(T, s & 0x7fffffff, p.sqdt, 0.0f);
+    L.x = s < 0 ? L.len : 0.0f;
   }
-  const float l = L.ep.x;
-  const float mu = drift(G, L.ep, L.e, L.x);
-  const float a = mu * L.dtr;
-  const float b = L.ep.w * L.sq * z;
-  const float xn = L.x + a + b;
-  if (xn > 0.0f && xn < l) {
+  const float mu = L.template drift<TAB>(G, L.x);
+  const float ss = L.sig * L.sq;
+  const float xn = fmaf(ss, z, fmaf(mu, L.dtr, L.x));
+  if (xn > 0.0f && xn < L.len) {
     L.x = xn;
     return true;
   }
   L.M += 1;
+  const float a = mu * L.dtr, b = ss * z;
   float s;
   if (xn <= 0.0f) {
-    s = solve_first_passage_s<float>(a, b, L.x);
+    s = solve_fast(a, b, L.x);
     L.x = 0.0f;
   } else {
-    s = solve_first_passage_s<float>(-a, -b, l - L.x);
-    L.x = l;
+    s = solve_fast(-a, -b, L.len - L.x);
+    L.x = L.len;
   }
   if (s < 0.0f) s = 1.0f;
   L.dtr = (1.0f - s * s) * L.dtr;
@@ -238,145 +351,149 @@ __device__ __forceinline__ bool general_trip(Lane &L, const NativeGraph &G, cons
     L.trunc = true;
     return true;
   }
-  L.sq = sqrtf(L.dtr);
+  L.sq = fast_sqrt(L.dtr);
   return false;
 }
 
-__device__ __forceinline__ Block native_block(uint64_t seed, uint32_t pair, uint32_t domain,
-                                              uint64_t id) {
-  return philox4x32_10(Block{pair, domain, (uint32_t)id, (uint32_t)(id >> 32)}, (uint32_t)seed,
-                       (uint32_t)(seed >> 32));
+template <bool STAR, bool SMEM, bool TAB>
+__device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
+                                          const Tables<SMEM> &T, const NatParams &p, float z,
+                                          uint32_t u, float mu) {
+  if constexpr (STAR)
+    return rare_star<SMEM, TAB>(L, G, T, p, z, u, mu);
+  else
+    return rare_general<SMEM, TAB>(L, G, T, p, z, u);
 }
 
-template <bool STAR>
-__device__ __forceinline__ void place_native(Lane &L, const NativeGraph &G, const Smem &S,
-                                             const NatParams &p, uint64_t id) {
+template <bool STAR, bool SMEM, bool TAB>
+__device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
+                                          const Tables<SMEM> &T, const NatParams &p, float z,
+                                          uint32_t u) {
+  return rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, L.template drift<TAB>(G, L.x));
+}
+
+// One trip for every lane of the warp.  `live` lanes advance; returns true for
+// lanes whose macro step completed.
+template <bool STAR, bool SMEM, bool TAB>
+__device__ __forceinline__ bool trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
+                                     const Tables<SMEM> &T, const Shared &S, const NatParams &p,
+                                     bool live, float z, uint32_t u) {
+  // common path: strictly inside the edge => fresh macro step (dtr == dt)
+  const float mu = L.template drift<TAB>(G, L.x);
+  const float xn = fmaf(L.sig_sqdt, z, fmaf(mu, p.dt, L.x));
+  bool ok = live && (L.x > 0.0f) && (xn > 0.0f) && (xn < L.len);
+  if (!STAR) ok = ok && (L.x < L.len);
+  L.x = ok ? xn : L.x;
+  bool done = ok;
+  if (live && !ok) {
+    done = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, mu);
+    if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
+  }
+  __syncwarp();
+  return done;
+}
+
+template <bool STAR, bool SMEM>
+__device__ __forceinline__ void place_native(Lane<STAR, SMEM> &L, const NativeGraph &G,
+                                             const Tables<SMEM> &T, const NatParams &p,
+                                             uint64_t id, float star_len) {
+  int e;
+  float x;
   if (p.init_kind == GSDE_INIT_POINT) {
-    L.e = p.init_edge;
-    L.x = p.init_x;
+    e = p.init_edge;
+    x = p.init_x;
   } else {
-    const Block r = native_block(p.seed, 0u, kDomainPlace, id);
+    const Block r = native_block(p, 0u, kDomainPlace, id);
     const double u = (double)((((uint64_t)r.x << 32) | r.y) >> 11) * kInv2p53;
     const double u2 = (double)((((uint64_t)r.z << 32) | r.w) >> 11) * kInv2p53;
-    int e = (int)(u * (double)G.n_edges);
+    e = (int)(u * (double)G.n_edges);
     if (e >= G.n_edges) e = G.n_edges - 1;
-    const double le = (double)S.edge[e].x;
-    L.e = e;
-    L.x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
+    const double le = (double)T.E(e).x;
+    x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
   }
-  L.ep = S.edge[L.e];
-  if (!STAR) L.ev = S.edgev[L.e];
+  L.load_edge(T, e, p.sqdt, star_len);
+  L.x = x;
+  L.dtr = p.dt;
+  L.sq = p.sqdt;
+  L.M = 0;
+  L.trunc = false;
+  L.steps_left = p.n_steps;
+  L.cross = L.events = L.truncs = 0;
 }
 
-template <bool STAR>
-__global__ void __launch_bounds__(kThreads) native_ensemble_kernel(NativeGraph G, NatParams p,
-                                                                  gsde_out o) {
+template <bool STAR, bool SMEM, bool TAB>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o) {
   const int nb = p.cap + 1;
-  const Smem S = smem_setup(G, nb, p.smem_graph, STAR);
+  Shared S;
+  Tables<SMEM> T;
+  shared_setup<STAR, SMEM>(G, nb, S, T, false);
+  const float star_len = p.reflect > 0.0f ? p.reflect : __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool active = i < p.n;
-  Lane L{};
-  int steps_left = p.n_steps;
-  int64_t cross = 0, events = 0, truncs = 0;
-  int64_t t_cross = 0, t_events = 0, t_trunc = 0;
+  Lane<STAR, SMEM> L;
+  L.x = 1.0f;
+  L.len = star_len;
+  L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
+  L.steps_left = 1;
   uint32_t pair = 0;
   uint64_t id = (uint64_t)(p.id_offset + i);
-  auto start = [&]() {
-    id = (uint64_t)(p.id_offset + i);
-    place_native<STAR>(L, G, S, p, id);
-    L.dtr = p.dt;
-    L.sq = p.sqdt;
-    L.M = 0;
-    L.trunc = false;
-    steps_left = p.n_steps;
-    cross = events = truncs = 0;
-    pair = 0;
-  };
+  if (active) place_native(L, G, T, p, id, star_len);
+
+  // finished particle: epilogue, then the next particle on a fresh block
   auto finish = [&]() {
-    t_cross += cross;
-    t_events += events;
-    t_trunc += truncs;
-    ensemble_epilogue(o, i, L.e, (double)L.x, cross, events, truncs);
+    atomicAdd(&S.tot[0], (unsigned long long)L.cross);
+    atomicAdd(&S.tot[1], (unsigned long long)L.events);
+    atomicAdd(&S.tot[2], (unsigned long long)L.truncs);
+    ensemble_epilogue(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     i += stride;
     active = i < p.n;
-    if (active) start();
+    pair = 0;
+    id = (uint64_t)(p.id_offset + i);
+    if (active) place_native(L, G, T, p, id, star_len);
   };
-  // one trip; returns true when the particle finished its last step
-  auto trip = [&](float z, uint32_t u) -> bool {
-    const bool done = STAR ? star_trip(L, G, S, p, z, u) : general_trip(L, G, S, p, z, u);
-    if (!done) return false;
-    if (L.M > 0) {
-      cross += L.M;
-      events += 1;
-      truncs += L.trunc ? 1 : 0;
-      mh_add(S, L.M > p.cap ? p.cap : L.M);
-    }
-    L.M = 0;
-    L.trunc = false;
-    L.dtr = p.dt;
-    L.sq = p.sqdt;
-    return --steps_left == 0;
-  };
-  if (active) {
-    start();
-    if (p.n_steps == 0) {  // placement only (engine.py:329-336)
-      while (active) finish();
-    }
-  }
+  if (p.n_steps == 0)
+    while (active) finish();
+
   while (__any_sync(0xffffffffu, active)) {
-    if (active) {
-      const Block r = native_block(p.seed, pair++, kDomainEnsemble, id);
-      float z0, z1;
-      box_muller(r.x, r.y, z0, z1);
-      // a lane whose particle finishes on the first trip idles on the second
-      // so that the next particle starts on a fresh block (pair 0)
-      if (trip(z0, r.z) || trip(z1, r.w)) finish();
-    }
+    const Block r = native_block(p, pair++, kDomainEnsemble, id);
+    float z0, z1;
+    box_muller(r.x, r.y, z0, z1);
+    bool fin = false;
+    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active, z0, r.z)) fin = --L.steps_left == 0;
+    if (!fin && trip<STAR, SMEM, TAB>(L, G, T, S, p, active, z1, r.w)) fin = --L.steps_left == 0;
+    if (fin) finish();
+    __syncwarp();
   }
-  if (o.totals) {
-    warp_add_i64(&o.totals[0], t_cross);
-    warp_add_i64(&o.totals[1], t_events);
-    warp_add_i64(&o.totals[2], t_trunc);
-  }
-  mh_flush(S, nb, o.m_hist);
+  shared_flush(S, nb, o.m_hist, o.totals, 3);
 }
 
-// Vertex trials: one macro step per trial, started at the vertex
-// (kernels.py:447-521); fused exit counts and M histogram (incl. M = 0).
-template <bool STAR>
-__global__ void __launch_bounds__(kThreads) native_trials_kernel(NativeGraph G, NatParams p,
-                                                                gsde_trials_out o, int priv_exit) {
+// Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
+// fused exit counts per edge and M histogram including M = 0.
+template <bool STAR, bool SMEM, bool TAB>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv) {
   const int nb = p.cap + 1;
-  const Smem S = smem_setup(G, nb, p.smem_graph, STAR);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // lane-private exit counters live after the staged graph (host sized it)
-  int *s_exit = nullptr;
-  if (priv_exit) {
-    size_t off = align16((size_t)(kPriv * kThreads + nb) * sizeof(int));
-    if (p.smem_graph)
-      off += (size_t)G.n_edges * (STAR ? 16 : 32) + (size_t)G.n_slots * 16;
-    s_exit = reinterpret_cast<int *>(smem_raw + off);
-    for (int j = threadIdx.x; j < G.n_edges * kThreads; j += blockDim.x) s_exit[j] = 0;
-    __syncthreads();
-  }
+  Shared S;
+  Tables<SMEM> T;
+  shared_setup<STAR, SMEM>(G, nb, S, T, exit_priv != 0);
+  const float inf = __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool active = i < p.n;
-  Lane L{};
+  Lane<STAR, SMEM> L;
   uint32_t pair = 0;
   uint64_t id = 0;
-  int64_t t_M = 0, t_ev = 0, t_tr = 0;
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
-    L.e = STAR ? 0 : p.start_edge;
+    L.load_edge(T, STAR ? 0 : p.start_edge, p.sqdt, inf);
     L.x = STAR ? 0.0f : p.start_x;
-    L.ep = S.edge[L.e];
-    if (!STAR) L.ev = S.edgev[L.e];
     L.dtr = p.dt;
     L.sq = p.sqdt;
     L.M = 0;
     L.trunc = false;
+    L.cross = L.events = L.truncs = 0;
     pair = 0;
   };
   auto finish = [&]() {
@@ -384,39 +501,41 @@ __global__ void __launch_bounds__(kThreads) native_trials_kernel(NativeGraph G, 
     if (o.edge) o.edge[i] = L.e;
     if (o.x) o.x[i] = (double)L.x;
     if (o.trunc) o.trunc[i] = L.trunc ? 1 : 0;
-    if (s_exit)
-      s_exit[L.e * kThreads + threadIdx.x] += 1;
+    if (S.exit_priv)
+      S.exit_priv[L.e * kThreads + threadIdx.x] += 1;
     else if (o.exit_counts)
       add_i64(&o.exit_counts[L.e], 1);
     mh_add(S, L.M > p.cap ? p.cap : L.M);
-    t_M += L.M;
-    t_ev += L.M > 0;
-    t_tr += L.trunc;
+    atomicAdd(&S.tot[0], (unsigned long long)L.M);
+    if (L.M > 0) atomicAdd(&S.tot[1], 1ull);
+    if (L.trunc) atomicAdd(&S.tot[2], 1ull);
     i += stride;
     active = i < p.n;
     if (active) start();
   };
+  L.x = 1.0f;
+  L.len = inf;
+  L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
   if (active) start();
+  // a trial is exactly one macro step started at the vertex: every trip is a
+  // vertex / split trip, so the rare-path step functions run directly
   while (__any_sync(0xffffffffu, active)) {
-    if (active) {
-      const Block r = native_block(p.seed, pair++, kDomainTrials, id);
-      float z0, z1;
-      box_muller(r.x, r.y, z0, z1);
-      const bool d0 = STAR ? star_trip(L, G, S, p, z0, r.z) : general_trip(L, G, S, p, z0, r.z);
-      if (d0 || (STAR ? star_trip(L, G, S, p, z1, r.w) : general_trip(L, G, S, p, z1, r.w)))
-        finish();
-    }
+    const Block r = native_block(p, pair++, kDomainTrials, id);
+    float z0, z1;
+    box_muller(r.x, r.y, z0, z1);
+    bool fin = false;
+    if (active) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z0, r.z);
+    __syncwarp();
+    if (active && !fin) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z1, r.w);
+    __syncwarp();
+    if (fin) finish();
+    __syncwarp();
   }
-  if (o.totals) {
-    warp_add_i64(&o.totals[0], t_M);
-    warp_add_i64(&o.totals[1], t_ev);
-    warp_add_i64(&o.totals[2], t_tr);
-  }
-  mh_flush(S, nb, o.m_hist);
-  if (s_exit && o.exit_counts) {
+  shared_flush(S, nb, o.m_hist, o.totals, 3);
+  if (S.exit_priv && o.exit_counts) {
     for (int e = threadIdx.x; e < G.n_edges; e += blockDim.x) {
       int64_t v = 0;
-      for (int t = 0; t < kThreads; ++t) v += s_exit[e * kThreads + t];
+      for (int t = 0; t < kThreads; ++t) v += S.exit_priv[e * kThreads + t];
       if (v) add_i64(&o.exit_counts[e], v);
     }
   }
@@ -450,8 +569,9 @@ __global__ void __launch_bounds__(256) histogram_kernel(int64_t n, const int64_t
   }
 }
 
-size_t smem_bytes(const gsde_graph *g, int nb, int stage, bool priv_exit) {
+size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit) {
   size_t b = ((size_t)(kPriv * kThreads + nb) * sizeof(int) + 15) & ~size_t(15);
+  b += 4 * sizeof(unsigned long long);
   if (stage) b += (size_t)g->E * (g->is_star ? 16 : 32) + (size_t)g->S * 16;
   if (priv_exit) b += (size_t)g->E * kThreads * sizeof(int);
   return b;
@@ -467,71 +587,84 @@ int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items) {
   return (int)(need < full ? (need < 1 ? 1 : need) : full);
 }
 
-NatParams make_params(const gsde_graph *g, uint64_t seed, int64_t n, int64_t off, double dt,
-                      int32_t cap) {
+NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
   NatParams p{};
   p.seed = seed;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r, k0 += kPhiloxW0, k1 += kPhiloxW1) {
+    p.rk[2 * r] = k0;
+    p.rk[2 * r + 1] = k1;
+  }
   p.n = n;
   p.id_offset = off;
   p.cap = cap;
   p.dt = (float)dt;
   p.sqdt = sqrtf((float)dt);
-  p.smem_graph = g->nat_graph_smem > 0 ? 1 : 0;
   return p;
 }
 
-cudaError_t set_smem_attr(const void *fn, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+template <class K, class... Args>
+cudaError_t launch(K kernel, size_t smem, int device, int64_t n, cudaStream_t s, Args... args) {
+  if (smem > 48 * 1024) {
+    cudaError_t err =
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+  }
+  kernel<<<occupancy_grid(kernel, smem, device, n), kThreads, smem, s>>>(args...);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Runtime flags -> compile-time kernel variant.
+template <class F>
+cudaError_t dispatch3(bool a, bool b, bool c, F &&f) {
+  using T = std::true_type;
+  using N = std::false_type;
+  if (a) {
+    if (b) return c ? f(T{}, T{}, T{}) : f(T{}, T{}, N{});
+    return c ? f(T{}, N{}, T{}) : f(T{}, N{}, N{});
+  }
+  if (b) return c ? f(N{}, T{}, T{}) : f(N{}, T{}, N{});
+  return c ? f(N{}, N{}, T{}) : f(N{}, N{}, N{});
 }
 
 }  // namespace
 
 cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const gsde_out &o,
                                    cudaStream_t s) {
-  NatParams p = make_params(g, a.seed, a.n_particles, a.pid_offset, a.dt, a.cap);
+  NatParams p = make_params(a.seed, a.n_particles, a.pid_offset, a.dt, a.cap);
   p.n_steps = (int32_t)a.n_steps;
   p.reflect = (float)a.reflect_len;
   p.init_kind = a.init_kind;
   p.init_edge = (int32_t)a.init_edge;
   p.init_x = (float)a.init_x;
   p.init_xmax = a.init_xmax;
-  const size_t smem = smem_bytes(g, a.cap + 1, p.smem_graph, false);
-  cudaError_t err;
-  if (g->is_star) {
-    auto k = native_ensemble_kernel<true>;
-    if ((err = set_smem_attr((const void *)k, smem)) != cudaSuccess) return err;
-    k<<<occupancy_grid(k, smem, g->device, a.n_particles), kThreads, smem, s>>>(g->nat, p, o);
-  } else {
-    auto k = native_ensemble_kernel<false>;
-    if ((err = set_smem_attr((const void *)k, smem)) != cudaSuccess) return err;
-    k<<<occupancy_grid(k, smem, g->device, a.n_particles), kThreads, smem, s>>>(g->nat, p, o);
-  }
-  count_launch();
-  return cudaGetLastError();
+  const bool stage = g->nat_graph_smem > 0;
+  const size_t smem = smem_bytes(g, a.cap + 1, stage, false);
+  const int d = g->device;
+  const int64_t n = a.n_particles;
+  return dispatch3(g->is_star, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
+    return launch(native_ensemble_kernel<decltype(star)::value, decltype(sm)::value,
+                                         decltype(tab)::value>,
+                  smem, d, n, s, g->nat, p, o);
+  });
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
                                  const gsde_trials_out &o, cudaStream_t s) {
-  NatParams p = make_params(g, a.seed, a.n_trials, a.trial_offset, a.dt, a.cap);
+  NatParams p = make_params(a.seed, a.n_trials, a.trial_offset, a.dt, a.cap);
   p.start_edge = (int32_t)a.start_edge;
   p.start_x = (float)a.start_x;
-  const int priv_exit = (o.exit_counts && g->E <= 32) ? 1 : 0;
-  const size_t smem = smem_bytes(g, a.cap + 1, p.smem_graph, priv_exit);
-  cudaError_t err;
-  if (g->is_star) {
-    auto k = native_trials_kernel<true>;
-    if ((err = set_smem_attr((const void *)k, smem)) != cudaSuccess) return err;
-    k<<<occupancy_grid(k, smem, g->device, a.n_trials), kThreads, smem, s>>>(g->nat, p, o,
-                                                                              priv_exit);
-  } else {
-    auto k = native_trials_kernel<false>;
-    if ((err = set_smem_attr((const void *)k, smem)) != cudaSuccess) return err;
-    k<<<occupancy_grid(k, smem, g->device, a.n_trials), kThreads, smem, s>>>(g->nat, p, o,
-                                                                              priv_exit);
-  }
-  count_launch();
-  return cudaGetLastError();
+  const int priv = (o.exit_counts && g->E <= 32) ? 1 : 0;
+  const bool stage = g->nat_graph_smem > 0;
+  const size_t smem = smem_bytes(g, a.cap + 1, stage, priv);
+  const int d = g->device;
+  const int64_t n = a.n_trials;
+  return dispatch3(g->is_star, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
+    return launch(native_trials_kernel<decltype(star)::value, decltype(sm)::value,
+                                       decltype(tab)::value>,
+                  smem, d, n, s, g->nat, p, o, priv);
+  });
 }
 
 cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,
