@@ -460,9 +460,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const Block r = native_block(p, pair++, kDomainEnsemble, id);
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
+    // trip() reconverges the warp internally: every lane must call it
     bool fin = false;
     if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active, z0, r.z)) fin = --L.steps_left == 0;
-    if (!fin && trip<STAR, SMEM, TAB>(L, G, T, S, p, active, z1, r.w)) fin = --L.steps_left == 0;
+    const bool live1 = active && !fin;
+    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, live1, z1, r.w)) fin = --L.steps_left == 0;
     if (fin) finish();
     __syncwarp();
   }
