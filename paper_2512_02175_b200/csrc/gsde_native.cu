@@ -74,7 +74,7 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, fl
   const float u1 = fmaf((float)a, 0x1p-32f, 0x1p-33f);
   const float r = fast_sqrt(fmaxf(fast_lg2(u1) * -1.3862943611198906f, 0.0f));  // -2 ln u1
   float s, c;
-  __sincosf((float)(int32_t)b * 7.3145904512e-10f, &s, &c);  // pi * 2^-31
+  __sincosf((float)(int32_t)b * 1.4629180792671596e-9f, &s, &c);  // pi * 2^-31
   z0 = r * c;
   z1 = r * s;
 }
