@@ -79,29 +79,28 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, fl
   z1 = r * s;
 }
 
-// kernels.py:88-131 in FP32 with approximate division / square root.
-__device__ __forceinline__ float solve_fast(float a, float b, float c) {
-  if (c < 0.0f) return 0.0f;
-  if (c == 0.0f) {
-    if (b <= 0.0f) return 0.0f;
-    if (a >= 0.0f) return -1.0f;
-    return fminf(__fdividef(-b, a), 1.0f);
-  }
-  if (a == 0.0f) {
-    if (b >= 0.0f) return -1.0f;
-    return fminf(__fdividef(-c, b), 1.0f);
-  }
-  const float disc = fmaxf(b * b - 4.0f * a * c, 0.0f);
-  const float sq = fast_sqrt(disc);
-  const float q = b >= 0.0f ? -0.5f * (b + sq) : -0.5f * (b - sq);
-  float s = -1.0f;
-  const float r1 = __fdividef(q, a);
-  if (r1 >= 0.0f) s = r1;
-  if (q != 0.0f) {
-    const float r2 = __fdividef(c, q);
-    if (r2 >= 0.0f && (s < 0.0f || r2 < s)) s = r2;
-  }
-  return s < 0.0f ? -1.0f : fminf(s, 1.0f);
+__device__ __forceinline__ float fast_rcp(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// kernels.py:88-131 in FP32, branch-free: first s >= 0 with a s^2 + b s + c = 0,
+// clamped to 1; -1 if none.  c < 0 -> 0; c == 0 -> 0 if b <= 0, else the
+// nonzero root -b/a when a < 0, else -1; otherwise the smallest nonnegative
+// of the stable pair q/a, c/q with q = -(b + sign(b) sqrt(disc)) / 2 (a = 0
+// falls out as q/a = +-inf, c/q = -c/b).
+__device__ __forceinline__ float solve_bf(float a, float b, float c) {
+  const float inf = __int_as_float(0x7f800000);
+  const float sq = fast_sqrt(fmaxf(b * b - 4.0f * a * c, 0.0f));
+  const float q = -0.5f * (b + copysignf(sq, b));
+  const float ra = fast_rcp(a);
+  const float r1 = q * ra;
+  const float r2 = c * fast_rcp(q);
+  float s = fminf(r1 >= 0.0f ? r1 : inf, (q != 0.0f && r2 >= 0.0f) ? r2 : inf);
+  s = s == inf ? -1.0f : fminf(s, 1.0f);
+  const float s0 = b <= 0.0f ? 0.0f : (a >= 0.0f ? -1.0f : fminf(-b * ra, 1.0f));
+  return c < 0.0f ? 0.0f : (c == 0.0f ? s0 : s);
 }
 
 // Philox4x32-10 with the key schedule precomputed in the kernel parameters:
@@ -231,6 +230,8 @@ struct Lane {
   float dtr, sq;   // time left in the current macro step and its sqrt
   int M;           // vertex resolutions in the current macro step
   bool trunc;
+  bool pend;       // a hit whose split time is not yet resolved
+  float pa, pb, pc;  // its first-passage quadratic (a, b, c)
   float mu_a, mu_b, sig, sig_sqdt;  // cached drift / diffusion of e
   float len;       // edge length (star: mirror wall or +inf)
   int4 ev;         // endpoint alias info of e (general graphs)
@@ -272,28 +273,36 @@ struct Lane {
     dtr = dt;
     sq = sqdt;
   }
+
+  __device__ __forceinline__ void set_hit(float a, float b, float c, float at) {
+    pend = true;
+    pa = a;
+    pb = b;
+    pc = c;
+    x = at;
+  }
 };
 
-// Rare trip of a star graph (kernels.py:146-220 semantics).  Returns true when
-// the macro step completed.
+// Rare trip of a star graph (kernels.py:146-220).  Lanes arrive here at the
+// vertex (x == 0, possibly with an unresolved overshoot from the previous
+// trip) or beyond the optional mirror wall.  Returns true when the macro
+// step completed.
 template <bool SMEM, bool TAB>
 __device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph &G,
-                                          const Tables<SMEM> &T, const NatParams &p,
-                                          float z, uint32_t u, float mu) {
-  if (L.x > 0.0f) {  // free step from the interior (dtr == dt)
-    const float xn = fmaf(L.sig_sqdt, z, fmaf(mu, p.dt, L.x));
-    if (xn > 0.0f) {  // beyond the mirror wall
-      L.x = fmaxf(2.0f * p.reflect - xn, 0.0f);
-      return true;
-    }
-    float s = solve_fast(mu * p.dt, L.sig_sqdt * z, L.x);
-    if (s < 0.0f) s = 1.0f;
-    L.dtr = fmaxf((1.0f - s * s) * p.dt, 0.0f);
-    L.sq = fast_sqrt(L.dtr);
-    L.x = 0.0f;
-    return false;
+                                          const Tables<SMEM> &T, const NatParams &p, float z,
+                                          uint32_t u, float xn_main) {
+  if (L.x > 0.0f) {  // free step beyond the mirror wall (kernels.py:185-188)
+    L.x = fmaxf(2.0f * p.reflect - xn_main, 0.0f);
+    return true;
   }
-  // at the vertex: sample the exit edge, one-sided |W| excursion
+  if (L.pend) {  // split the overshooting free step at the vertex (kernels.py:190-195)
+    float s = solve_bf(L.pa, L.pb, L.pc);
+    s = s < 0.0f ? 1.0f : s;
+    L.dtr = fmaxf((1.0f - s * s) * L.dtr, 0.0f);
+    L.sq = fast_sqrt(L.dtr);
+    L.pend = false;
+  }
+  // sample the exit edge, one-sided |W| excursion (kernels.py:198-220)
   L.M += 1;
   L.load_edge(T, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
   const float w = fabsf(z);
@@ -303,7 +312,7 @@ __device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph
     L.x = (p.reflect > 0.0f && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
     return true;
   }
-  const float alpha = __fdividef(w * w * L.sig * L.sig, mu0 * mu0 * L.dtr);
+  const float alpha = (w * w * L.sig * L.sig) * fast_rcp(mu0 * mu0 * L.dtr);
   L.dtr = (1.0f - alpha) * L.dtr;
   L.x = 0.0f;
   if (L.dtr <= 0.0f) return true;
@@ -315,81 +324,91 @@ __device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph
   return false;
 }
 
-// Rare trip of a general graph (kernels.py:223-288 semantics).
+// Rare trip of a general graph (kernels.py:223-288).  Lanes arrive here at a
+// vertex: first resolve a pending hit (residual time, stop / cap checks),
+// then resample the exit slot and propose from the new edge's endpoint.
 template <bool SMEM, bool TAB>
 __device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeGraph &G,
                                              const Tables<SMEM> &T, const NatParams &p,
                                              float z, uint32_t u) {
-  const bool at_init = !(L.x > 0.0f);
-  const bool at_term = !(L.x < L.len);  // (x == len exactly: the far vertex)
-  if (at_init || at_term) {  // resample the exit slot at the hit vertex
-    const int s = alias_pick(T, at_init ? L.ev.x : L.ev.z, at_init ? L.ev.y : L.ev.w, u);
-    L.load_edge(T, s & 0x7fffffff, p.sqdt, 0.0f);
-    L.x = s < 0 ? L.len : 0.0f;
+  if (L.pend) {
+    float s = solve_bf(L.pa, L.pb, L.pc);
+    s = s < 0.0f ? 1.0f : s;
+    L.dtr = (1.0f - s * s) * L.dtr;
+    L.pend = false;
+    if (L.dtr <= 0.0f) return true;  // step ends at the vertex, on the old edge
+    if (L.M >= p.cap) {
+      L.trunc = true;
+      return true;
+    }
+    L.sq = fast_sqrt(L.dtr);
   }
+  const bool at_init = !(L.x > 0.0f);
+  const int s = alias_pick(T, at_init ? L.ev.x : L.ev.z, at_init ? L.ev.y : L.ev.w, u);
+  L.load_edge(T, s & 0x7fffffff, p.sqdt, 0.0f);
+  L.x = s < 0 ? L.len : 0.0f;
   const float mu = L.template drift<TAB>(G, L.x);
-  const float ss = L.sig * L.sq;
-  const float xn = fmaf(ss, z, fmaf(mu, L.dtr, L.x));
+  const float a = mu * L.dtr;
+  const float b = (L.sig * L.sq) * z;
+  const float xn = L.x + a + b;
   if (xn > 0.0f && xn < L.len) {
     L.x = xn;
     return true;
   }
   L.M += 1;
-  const float a = mu * L.dtr, b = ss * z;
-  float s;
-  if (xn <= 0.0f) {
-    s = solve_fast(a, b, L.x);
-    L.x = 0.0f;
-  } else {
-    s = solve_fast(-a, -b, L.len - L.x);
-    L.x = L.len;
-  }
-  if (s < 0.0f) s = 1.0f;
-  L.dtr = (1.0f - s * s) * L.dtr;
-  if (L.dtr <= 0.0f) return true;
-  if (L.M >= p.cap) {
-    L.trunc = true;
-    return true;
-  }
-  L.sq = fast_sqrt(L.dtr);
+  if (xn <= 0.0f)
+    L.set_hit(a, b, L.x, 0.0f);
+  else
+    L.set_hit(-a, -b, L.len - L.x, L.len);
   return false;
 }
 
 template <bool STAR, bool SMEM, bool TAB>
 __device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
                                           const Tables<SMEM> &T, const NatParams &p, float z,
-                                          uint32_t u, float mu) {
+                                          uint32_t u, float xn_main) {
   if constexpr (STAR)
-    return rare_star<SMEM, TAB>(L, G, T, p, z, u, mu);
+    return rare_star<SMEM, TAB>(L, G, T, p, z, u, xn_main);
   else
     return rare_general<SMEM, TAB>(L, G, T, p, z, u);
 }
 
-template <bool STAR, bool SMEM, bool TAB>
-__device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
-                                          const Tables<SMEM> &T, const NatParams &p, float z,
-                                          uint32_t u) {
-  return rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, L.template drift<TAB>(G, L.x));
-}
-
 // One trip for every lane of the warp.  `live` lanes advance; returns true for
 // lanes whose macro step completed.
+//
+// Common path: a lane strictly inside its edge always starts a fresh macro
+// step (dtr == dt), so the proposal uses cached constants.  Accepted: done.
+// Overshoot at an end: the hit is recorded (x = vertex, quadratic saved) with
+// predicated moves; its split time is solved by the next (vertex) trip, so
+// all vertex work is one divergent region per trip.
 template <bool STAR, bool SMEM, bool TAB>
 __device__ __forceinline__ bool trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
                                      const Tables<SMEM> &T, const Shared &S, const NatParams &p,
                                      bool live, float z, uint32_t u) {
-  // common path: strictly inside the edge => fresh macro step (dtr == dt)
   const float mu = L.template drift<TAB>(G, L.x);
-  const float xn = fmaf(L.sig_sqdt, z, fmaf(mu, p.dt, L.x));
-  bool ok = live && (L.x > 0.0f) && (xn > 0.0f) && (xn < L.len);
-  if (!STAR) ok = ok && (L.x < L.len);
+  const float a = mu * p.dt;
+  const float b = L.sig_sqdt * z;
+  const float xn = L.x + a + b;
+  const bool inside = STAR ? (L.x > 0.0f) : (L.x > 0.0f && L.x < L.len);
+  const bool lo_ok = xn > 0.0f, hi_ok = xn < L.len;
+  const bool run = live && inside;
+  const bool ok = run && lo_ok && hi_ok;
+  const bool hit_lo = run && !lo_ok;
+  const bool hit_hi = !STAR && run && lo_ok && !hi_ok;
+  if (hit_lo || hit_hi) {
+    if (!STAR) L.M += 1;  // general counts hits; star counts vertex iterations
+    L.pend = true;
+    L.pa = hit_lo ? a : -a;
+    L.pb = hit_lo ? b : -b;
+    L.pc = hit_lo ? L.x : L.len - L.x;
+    L.x = hit_lo ? 0.0f : L.len;
+  }
   L.x = ok ? xn : L.x;
   bool done = ok;
-  if (live && !ok) {
-    done = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, mu);
+  if (live && !ok && !(hit_lo || hit_hi)) {
+    done = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, xn);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
-  __syncwarp();
   return done;
 }
 
@@ -417,6 +436,7 @@ __device__ __forceinline__ void place_native(Lane<STAR, SMEM> &L, const NativeGr
   L.sq = p.sqdt;
   L.M = 0;
   L.trunc = false;
+  L.pend = false;
   L.steps_left = p.n_steps;
   L.cross = L.events = L.truncs = 0;
 }
@@ -436,16 +456,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   L.x = 1.0f;
   L.len = star_len;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
+  L.pend = false;
+  L.M = 0;
   L.steps_left = 1;
   uint32_t pair = 0;
   uint64_t id = (uint64_t)(p.id_offset + i);
+  int64_t t_cross = 0, t_events = 0, t_truncs = 0;
   if (active) place_native(L, G, T, p, id, star_len);
 
   // finished particle: epilogue, then the next particle on a fresh block
   auto finish = [&]() {
-    atomicAdd(&S.tot[0], (unsigned long long)L.cross);
-    atomicAdd(&S.tot[1], (unsigned long long)L.events);
-    atomicAdd(&S.tot[2], (unsigned long long)L.truncs);
+    t_cross += L.cross;
+    t_events += L.events;
+    t_truncs += L.truncs;
     ensemble_epilogue(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     i += stride;
     active = i < p.n;
@@ -460,15 +483,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const Block r = native_block(p, pair++, kDomainEnsemble, id);
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
-    // trip() reconverges the warp internally: every lane must call it
     bool fin = false;
     if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active, z0, r.z)) fin = --L.steps_left == 0;
-    const bool live1 = active && !fin;
-    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, live1, z1, r.w)) fin = --L.steps_left == 0;
+    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active && !fin, z1, r.w))
+      fin = --L.steps_left == 0;
     if (fin) finish();
-    __syncwarp();
   }
-  shared_flush(S, nb, o.m_hist, o.totals, 3);
+  if (o.totals) {
+    warp_add_i64(&o.totals[0], t_cross);
+    warp_add_i64(&o.totals[1], t_events);
+    warp_add_i64(&o.totals[2], t_truncs);
+  }
+  shared_flush(S, nb, o.m_hist, nullptr, 0);
 }
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
@@ -487,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   Lane<STAR, SMEM> L;
   uint32_t pair = 0;
   uint64_t id = 0;
+  int64_t t_M = 0, t_ev = 0, t_tr = 0;
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
     L.load_edge(T, STAR ? 0 : p.start_edge, p.sqdt, inf);
@@ -495,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     L.sq = p.sqdt;
     L.M = 0;
     L.trunc = false;
-    L.cross = L.events = L.truncs = 0;
+    L.pend = false;
     pair = 0;
   };
   auto finish = [&]() {
@@ -508,9 +535,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     else if (o.exit_counts)
       add_i64(&o.exit_counts[L.e], 1);
     mh_add(S, L.M > p.cap ? p.cap : L.M);
-    atomicAdd(&S.tot[0], (unsigned long long)L.M);
-    if (L.M > 0) atomicAdd(&S.tot[1], 1ull);
-    if (L.trunc) atomicAdd(&S.tot[2], 1ull);
+    t_M += L.M;
+    t_ev += L.M > 0 ? 1 : 0;
+    t_tr += L.trunc ? 1 : 0;
     i += stride;
     active = i < p.n;
     if (active) start();
@@ -519,21 +546,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   L.len = inf;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
   if (active) start();
-  // a trial is exactly one macro step started at the vertex: every trip is a
-  // vertex / split trip, so the rare-path step functions run directly
+  // a trial is one macro step started at the vertex: every trip is a vertex
+  // trip, so the rare-path step functions run directly
   while (__any_sync(0xffffffffu, active)) {
     const Block r = native_block(p, pair++, kDomainTrials, id);
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
     bool fin = false;
-    if (active) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z0, r.z);
-    __syncwarp();
-    if (active && !fin) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z1, r.w);
-    __syncwarp();
+    if (active) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z0, r.z, 0.0f);
+    if (active && !fin) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z1, r.w, 0.0f);
     if (fin) finish();
-    __syncwarp();
   }
-  shared_flush(S, nb, o.m_hist, o.totals, 3);
+  if (o.totals) {
+    warp_add_i64(&o.totals[0], t_M);
+    warp_add_i64(&o.totals[1], t_ev);
+    warp_add_i64(&o.totals[2], t_tr);
+  }
+  shared_flush(S, nb, o.m_hist, nullptr, 0);
   if (S.exit_priv && o.exit_counts) {
     for (int e = threadIdx.x; e < G.n_edges; e += blockDim.x) {
       int64_t v = 0;
