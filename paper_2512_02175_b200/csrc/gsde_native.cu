@@ -25,6 +25,7 @@
 //    histogram in the particle epilogue.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "gsde_epilogue.cuh"
@@ -54,6 +55,7 @@ struct NatParams {
   double init_xmax;
   int32_t start_edge; // trials (general)
   float start_x;
+  int32_t rare_q;     // vertex trips only on trips t with t % rare_q == 0 (power of 2)
 };
 
 __device__ __forceinline__ float fast_sqrt(float v) {
@@ -384,7 +386,7 @@ __device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph
 template <bool STAR, bool SMEM, bool TAB>
 __device__ __forceinline__ bool trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
                                      const Tables<SMEM> &T, const Shared &S, const NatParams &p,
-                                     bool live, float z, uint32_t u) {
+                                     bool live, bool vertex_slot, float z, uint32_t u) {
   const float mu = L.template drift<TAB>(G, L.x);
   const float a = mu * p.dt;
   const float b = L.sig_sqdt * z;
@@ -405,7 +407,10 @@ __device__ __forceinline__ bool trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
   }
   L.x = ok ? xn : L.x;
   bool done = ok;
-  if (live && !ok && !(hit_lo || hit_hi)) {
+  // lanes at a vertex wait for their next vertex slot (deterministic per
+  // particle: slots depend only on the particle's own trip counter); a star
+  // proposal beyond the mirror wall is resolved at once
+  if (live && !ok && !(hit_lo || hit_hi) && (vertex_slot || (STAR && L.x > 0.0f))) {
     done = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, xn);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
@@ -451,7 +456,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const float star_len = p.reflect > 0.0f ? p.reflect : __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool active = i < p.n;
   Lane<STAR, SMEM> L;
   L.x = 1.0f;
   L.len = star_len;
@@ -460,32 +464,49 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   L.M = 0;
   L.steps_left = 1;
   uint32_t pair = 0;
-  uint64_t id = (uint64_t)(p.id_offset + i);
+  uint64_t id = 0;
   int64_t t_cross = 0, t_events = 0, t_truncs = 0;
-  if (active) place_native(L, G, T, p, id, star_len);
+  // particles start only on warp iterations that are multiples of the
+  // vertex-slot period, so the lanes of a warp share their slot phase
+  const uint32_t q = (uint32_t)p.rare_q;
+  const uint32_t period = q > 2 ? q / 2 : 1;  // in trip pairs
+  bool waiting = i < p.n;                     // next particle not started yet
+  bool active = false;                        // a particle is in flight
 
-  // finished particle: epilogue, then the next particle on a fresh block
   auto finish = [&]() {
     t_cross += L.cross;
     t_events += L.events;
     t_truncs += L.truncs;
     ensemble_epilogue(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     i += stride;
-    active = i < p.n;
-    pair = 0;
-    id = (uint64_t)(p.id_offset + i);
-    if (active) place_native(L, G, T, p, id, star_len);
+    active = false;
+    waiting = i < p.n;
   };
-  if (p.n_steps == 0)
-    while (active) finish();
+  if (p.n_steps == 0) {  // placement only (engine.py:329-336)
+    while (waiting) {
+      id = (uint64_t)(p.id_offset + i);
+      place_native(L, G, T, p, id, star_len);
+      finish();
+    }
+  }
 
-  while (__any_sync(0xffffffffu, active)) {
+  for (uint32_t it = 0; __any_sync(0xffffffffu, active || waiting); ++it) {
+    if (waiting && (it & (period - 1)) == 0) {
+      id = (uint64_t)(p.id_offset + i);
+      place_native(L, G, T, p, id, star_len);
+      pair = 0;
+      waiting = false;
+      active = true;
+    }
+    const uint32_t t0 = 2 * pair;
     const Block r = native_block(p, pair++, kDomainEnsemble, id);
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
     bool fin = false;
-    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active, z0, r.z)) fin = --L.steps_left == 0;
-    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active && !fin, z1, r.w))
+    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active, (t0 & (q - 1)) == 0, z0, r.z))
+      fin = --L.steps_left == 0;
+    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active && !fin, ((t0 + 1) & (q - 1)) == 0, z1,
+                              r.w))
       fin = --L.steps_left == 0;
     if (fin) finish();
   }
@@ -618,9 +639,22 @@ int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items) {
   return (int)(need < full ? (need < 1 ? 1 : need) : full);
 }
 
+// Vertex-slot period of the ensemble kernel (power of two; GSDE_RARE_Q overrides).
+int32_t rare_period() {
+  static int32_t q = [] {
+    const char *e = getenv("GSDE_RARE_Q");
+    int v = e ? atoi(e) : 4;
+    int r = 1;
+    while (r < v && r < 64) r <<= 1;
+    return r;
+  }();
+  return q;
+}
+
 NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
   NatParams p{};
   p.seed = seed;
+  p.rare_q = 1;
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   for (int r = 0; r < 10; ++r, k0 += kPhiloxW0, k1 += kPhiloxW1) {
     p.rk[2 * r] = k0;
@@ -670,6 +704,7 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   p.init_edge = (int32_t)a.init_edge;
   p.init_x = (float)a.init_x;
   p.init_xmax = a.init_xmax;
+  p.rare_q = rare_period();
   const bool stage = g->nat_graph_smem > 0;
   const size_t smem = smem_bytes(g, a.cap + 1, stage, false);
   const int d = g->device;
