@@ -136,6 +136,55 @@ double orc_u64_to_normal(uint64_t r) {
   return norm_ppf_qt(q, pt);
 }
 
+/* ---- draw lookahead buffer (kernels.py:46, :55-64): value-neutral ---------- */
+#define ORC_BUF 64
+typedef struct {
+  uint64_t seed, pid, k, kbase;
+  uint64_t buf[ORC_BUF];
+} orc_draws;
+
+/* Refill: ORC_BUF independent Philox evaluations in a branch-free loop the
+ * compiler vectorises (the reference's numba loop is vectorised the same way). */
+__attribute__((target_clones("avx512f", "avx2", "default")))
+static void draws_refill(orc_draws *d) {
+  const uint64_t base = d->k;
+  const uint32_t s0 = (uint32_t)d->seed, s1 = (uint32_t)(d->seed >> 32);
+  const uint32_t p0 = (uint32_t)d->pid, p1 = (uint32_t)(d->pid >> 32);
+  for (int j = 0; j < ORC_BUF; ++j) {
+    const uint64_t idx = base + (uint64_t)j;
+    const uint64_t blk = idx >> 1;
+    uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32), c2 = p0, c3 = p1;
+    uint32_t k0 = s0, k1 = s1;
+    for (int r = 0; r < 10; ++r) {
+      const uint64_t q0 = (uint64_t)PH_M0 * c0;
+      const uint64_t q1 = (uint64_t)PH_M1 * c2;
+      const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1 ^ k0;
+      const uint32_t n2 = (uint32_t)(q0 >> 32) ^ c3 ^ k1;
+      c1 = (uint32_t)q1;
+      c3 = (uint32_t)q0;
+      c0 = n0;
+      c2 = n2;
+      k0 += PH_W0;
+      k1 += PH_W1;
+    }
+    const uint64_t even = ((uint64_t)c0 << 32) | c1, odd = ((uint64_t)c2 << 32) | c3;
+    d->buf[j] = (idx & 1u) ? odd : even;
+  }
+  d->kbase = base;
+}
+
+static inline uint64_t draw(orc_draws *d) {
+  if (d->k - d->kbase >= ORC_BUF) draws_refill(d);
+  return d->buf[d->k++ - d->kbase];
+}
+
+static inline void draws_init(orc_draws *d, uint64_t seed, uint64_t pid, uint64_t k) {
+  d->seed = seed;
+  d->pid = pid;
+  d->k = k;
+  d->kbase = k - ORC_BUF; /* empty: first draw refills */
+}
+
 /* ---- packed graph + field (graph.py:102-125, coefficients.py:121-152) -- */
 typedef struct {
   int64_t n_edges, n_vertices;
@@ -212,12 +261,11 @@ typedef struct {
 
 /* kernels.py:146-220 (draws: N on a free step; then U,N per vertex iteration) */
 static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double dt,
-                              uint64_t seed, uint64_t pid, uint64_t k, int64_t cap,
-                              double reflect_len) {
+                              orc_draws *d, int64_t cap, double reflect_len) {
   orc_step_out o;
   int64_t M = 0;
   if (x > 0.0) {
-    double w = orc_u64_to_normal(orc_raw64(seed, pid, k++));
+    double w = orc_u64_to_normal(draw(d));
     double mu = drift_at(g, edge, x);
     double a = mu * dt;
     double b = g->sigma[edge] * sqrt(dt) * w;
@@ -227,7 +275,7 @@ static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double
         xn = 2.0 * reflect_len - xn;
         if (xn < 0.0) xn = 0.0;
       }
-      o.edge = edge; o.x = xn; o.M = 0; o.trunc = 0; o.k = k;
+      o.edge = edge; o.x = xn; o.M = 0; o.trunc = 0; o.k = d->k;
       return o;
     }
     double s = orc_solve_first_passage_s(a, b, x);
@@ -237,9 +285,9 @@ static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double
   }
   for (;;) {
     ++M;
-    double u = orc_u64_to_uniform(orc_raw64(seed, pid, k++));
+    double u = orc_u64_to_uniform(draw(d));
     edge = g->v_edges[pick_slot(g, 0, u)];
-    double w = orc_u64_to_normal(orc_raw64(seed, pid, k++));
+    double w = orc_u64_to_normal(draw(d));
     double mu0 = drift_at(g, edge, 0.0);
     double sig0 = g->sigma[edge];
     double xn = mu0 * dt + sig0 * sqrt(dt) * fabs(w);
@@ -248,17 +296,17 @@ static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double
         xn = 2.0 * reflect_len - xn;
         if (xn < 0.0) xn = 0.0;
       }
-      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = k;
+      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = d->k;
       return o;
     }
     double alpha = (w * w * sig0 * sig0) / (mu0 * mu0 * dt);
     dt = (1.0 - alpha) * dt;
     if (dt <= 0.0) {
-      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 0; o.k = k;
+      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 0; o.k = d->k;
       return o;
     }
     if (M >= cap) {
-      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 1; o.k = k;
+      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 1; o.k = d->k;
       return o;
     }
   }
@@ -266,26 +314,26 @@ static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double
 
 /* kernels.py:223-288 (draws per iteration: [U if at a vertex], N) */
 static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, double dt,
-                                 uint64_t seed, uint64_t pid, uint64_t k, int64_t cap) {
+                                 orc_draws *d, int64_t cap) {
   orc_step_out o;
   int64_t M = 0;
   for (;;) {
     double l = g->edge_len[edge];
     if (x <= 0.0 || x >= l) {
       int64_t v = x <= 0.0 ? g->edge_init[edge] : g->edge_term[edge];
-      double u = orc_u64_to_uniform(orc_raw64(seed, pid, k++));
+      double u = orc_u64_to_uniform(draw(d));
       int64_t slot = pick_slot(g, v, u);
       edge = g->v_edges[slot];
       l = g->edge_len[edge];
       x = g->v_orient[slot] == 0 ? 0.0 : l;
     }
-    double w = orc_u64_to_normal(orc_raw64(seed, pid, k++));
+    double w = orc_u64_to_normal(draw(d));
     double mu = drift_at(g, edge, x);
     double a = mu * dt;
     double b = g->sigma[edge] * sqrt(dt) * w;
     double xn = x + a + b;
     if (0.0 < xn && xn < l) {
-      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = k;
+      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = d->k;
       return o;
     }
     ++M;
@@ -300,11 +348,11 @@ static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, dou
     if (s < 0.0) s = 1.0;
     dt = (1.0 - s * s) * dt;
     if (dt <= 0.0) {
-      o.edge = edge; o.x = x; o.M = M; o.trunc = 0; o.k = k;
+      o.edge = edge; o.x = x; o.M = M; o.trunc = 0; o.k = d->k;
       return o;
     }
     if (M >= cap) {
-      o.edge = edge; o.x = x; o.M = M; o.trunc = 1; o.k = k;
+      o.edge = edge; o.x = x; o.M = M; o.trunc = 1; o.k = d->k;
       return o;
     }
   }
@@ -314,8 +362,10 @@ static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, dou
 void orc_step(const orc_graph *g, int32_t star, int64_t edge, double x, double dt,
               uint64_t seed, uint64_t pid, uint64_t k, int64_t cap, double reflect_len,
               int64_t *o_edge, double *o_x, int64_t *o_M, int32_t *o_trunc, uint64_t *o_k) {
-  orc_step_out o = star ? step_star(g, edge, x, dt, seed, pid, k, cap, reflect_len)
-                        : step_general(g, edge, x, dt, seed, pid, k, cap);
+  orc_draws d;
+  draws_init(&d, seed, pid, k);
+  orc_step_out o = star ? step_star(g, edge, x, dt, &d, cap, reflect_len)
+                        : step_general(g, edge, x, dt, &d, cap);
   *o_edge = o.edge; *o_x = o.x; *o_M = o.M; *o_trunc = o.trunc; *o_k = o.k;
 }
 
@@ -358,11 +408,13 @@ void orc_ensemble(const orc_graph *g, int32_t star, uint64_t seed, int64_t n_par
       double x;
       uint64_t k;
       place(g, seed, pid, init_kind, init_edge, init_x, init_xmax, &edge, &x, &k);
+      orc_draws d;
+      draws_init(&d, seed, pid, k);
       int64_t cross = 0, events = 0, truncs = 0;
       for (int64_t s = 0; s < n_steps; ++s) {
-        orc_step_out o = star ? step_star(g, edge, x, dt, seed, pid, k, cap, reflect_len)
-                              : step_general(g, edge, x, dt, seed, pid, k, cap);
-        edge = o.edge; x = o.x; k = o.k;
+        orc_step_out o = star ? step_star(g, edge, x, dt, &d, cap, reflect_len)
+                              : step_general(g, edge, x, dt, &d, cap);
+        edge = o.edge; x = o.x;
         if (o.M > 0) {
           cross += o.M;
           events += 1;
@@ -390,8 +442,10 @@ void orc_vertex_trials(const orc_graph *g, int32_t star, uint64_t seed, int64_t 
 #endif
   for (int64_t i = 0; i < n_trials; ++i) {
     uint64_t pid = (uint64_t)(i + trial_offset);
-    orc_step_out o = star ? step_star(g, 0, 0.0, dt, seed, pid, 0, cap, 0.0)
-                          : step_general(g, start_edge, start_x, dt, seed, pid, 0, cap);
+    orc_draws d;
+    draws_init(&d, seed, pid, 0);
+    orc_step_out o = star ? step_star(g, 0, 0.0, dt, &d, cap, 0.0)
+                          : step_general(g, start_edge, start_x, dt, &d, cap);
     if (out_M) out_M[i] = o.M;
     if (out_edge) out_edge[i] = o.edge;
     if (out_x) out_x[i] = o.x;
