@@ -280,12 +280,8 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
         stats = BounceStats(np.zeros(cap + 1, np.int64), run_gamma, 0, 0, 0)
         return EnsembleResult(z, np.zeros(0), z.copy(), z.copy(), stats, config)
     res = ensemble_device(graph, field, config, outputs=("edge", "x", "crossings", "events"))
-    edges = res["edge"].cpu().numpy()
-    positions = res["x"].cpu().numpy()
-    crossings = res["crossings"].cpu().numpy()
-    events = res["events"].cpu().numpy()
-    m_hist = res["m_hist"].cpu().numpy()
-    totals = res["totals"].cpu().numpy()
+    edges, positions, crossings, events, m_hist, totals = _to_host(
+        [res[k] for k in ("edge", "x", "crossings", "events", "m_hist", "totals")])
     stats = BounceStats(
         m_histogram=m_hist,
         gamma=run_gamma,
@@ -300,6 +296,20 @@ def _bits64(v: int) -> int:
     """uint64 value as the int64 with the same bit pattern (torch storage)."""
     v = int(v) & 0xFFFFFFFFFFFFFFFF
     return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def _to_host(tensors):
+    """Device tensors -> numpy arrays through pinned staging buffers (torch's
+    caching host allocator recycles them across calls); one stream sync."""
+    import torch
+
+    hosts = []
+    for t in tensors:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        hosts.append(h)
+    torch.cuda.current_stream(tensors[0].device).synchronize()
+    return [h.numpy() for h in hosts]
 
 
 def _step(graph, field, state, dt, rng, max_splits, reflect_at, star):
@@ -466,8 +476,7 @@ def vertex_crossing_trials(graph: MetricGraph, field: CoefficientField, dt: floa
     n = int(n_trials)
     if n > 0:
         res = trials_device(graph, field, dt, n, seed, vertex, max_splits, rng, device)
-        M, ex, xs, tr = (res["M"].cpu().numpy(), res["edge"].cpu().numpy(),
-                         res["x"].cpu().numpy(), res["trunc"].cpu().numpy())
+        M, ex, xs, tr = _to_host([res["M"], res["edge"], res["x"], res["trunc"]])
     else:
         _trial_start(graph, vertex)
         M = np.zeros(0, np.int64)
