@@ -258,8 +258,9 @@ def load_traffic(workload):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get(workload)
-    except OSError:
+            entry = json.load(fh).get(workload)
+        return None if entry is None else entry["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
         return None
 
 

@@ -2,10 +2,18 @@
 import csv, json, subprocess, sys
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    return dict(zip(r[0], r[2]))
+    d = dict(zip(r[0], r[2]))
+    units = dict(zip(r[0], r[1]))
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if k in d:
+            d[k + ".bytes"] = float(d[k].replace(",", "")) * SCALE.get(units.get(k, "byte"), 1)
+    return d
 
 
 def summary(rep):
@@ -13,7 +21,7 @@ def summary(rep):
     keys = ['Kernel Name', 'gpu__time_duration.sum', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
             'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__inst_executed.avg.per_cycle_active',
             'sm__warps_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread',
-            'launch__grid_size', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+            'launch__grid_size', 'dram__bytes_read.sum.bytes', 'dram__bytes_write.sum.bytes',
             'smsp__thread_inst_executed_per_inst_executed.ratio',
             'sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active',
             'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active',
