@@ -74,7 +74,8 @@ __device__ __forceinline__ float fast_lg2(float v) {
 // (|z| <= 6.8), angle uniform on [-pi, pi).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = fmaf((float)a, 0x1p-32f, 0x1p-33f);
-  const float r = fast_sqrt(fmaxf(fast_lg2(u1) * -1.3862943611198906f, 0.0f));  // -2 ln u1
+  // u1 <= 1 so -2 ln u1 >= 0 (lg2.approx(1) == 0)
+  const float r = fast_sqrt(fast_lg2(u1) * -1.3862943611198906f);
   float s, c;
   __sincosf((float)(int32_t)b * 1.4629180792671596e-9f, &s, &c);  // pi * 2^-31
   z0 = r * c;
@@ -232,8 +233,8 @@ struct Lane {
   float dtr, sq;   // time left in the current macro step and its sqrt
   int M;           // vertex resolutions in the current macro step
   bool trunc;
-  bool pend;       // a hit whose split time is not yet resolved
-  float pa, pb, pc;  // its first-passage quadratic (a, b, c)
+  bool pend;       // a hit whose split time is not yet resolved:
+  float px, pz;    //   proposal start x and its Gaussian (a, b re-derived)
   float mu_a, mu_b, sig, sig_sqdt;  // cached drift / diffusion of e
   float len;       // edge length (star: mirror wall or +inf)
   int4 ev;         // endpoint alias info of e (general graphs)
@@ -262,6 +263,19 @@ struct Lane {
     return fmaf(mu_b, at, mu_a);
   }
 
+  // split time of the pending hit: the proposal x' = px + mu(px) dtr + sig sq pz
+  // left the edge through the vertex the lane now sits at (kernels.py:190-195,
+  // :276-283); residual time (1 - s^2) dtr
+  template <bool TAB>
+  __device__ __forceinline__ float split_factor(const NativeGraph &G) const {
+    const float a = drift<TAB>(G, px) * dtr;
+    const float b = (sig * sq) * pz;
+    const bool lo = STAR || !(x > 0.0f);
+    float s = lo ? solve_bf(a, b, px) : solve_bf(-a, -b, len - px);
+    s = s < 0.0f ? 1.0f : s;
+    return 1.0f - s * s;
+  }
+
   // macro step finished: statistics, reset for the next step
   __device__ __forceinline__ void step_done(const Shared &S, int cap, float dt, float sqdt) {
     if (M > 0) {
@@ -275,32 +289,22 @@ struct Lane {
     dtr = dt;
     sq = sqdt;
   }
-
-  __device__ __forceinline__ void set_hit(float a, float b, float c, float at) {
-    pend = true;
-    pa = a;
-    pb = b;
-    pc = c;
-    x = at;
-  }
 };
 
 // Rare trip of a star graph (kernels.py:146-220).  Lanes arrive here at the
-// vertex (x == 0, possibly with an unresolved overshoot from the previous
-// trip) or beyond the optional mirror wall.  Returns true when the macro
-// step completed.
-template <bool SMEM, bool TAB>
+// vertex (x == 0, possibly with an unresolved overshoot from an earlier trip)
+// or beyond the optional mirror wall.  Returns true when the macro step
+// completed.
+template <bool SMEM, bool TAB, bool REFLECT>
 __device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph &G,
                                           const Tables<SMEM> &T, const NatParams &p, float z,
                                           uint32_t u, float xn_main) {
-  if (L.x > 0.0f) {  // free step beyond the mirror wall (kernels.py:185-188)
+  if (REFLECT && L.x > 0.0f) {  // free step beyond the mirror wall (kernels.py:185-188)
     L.x = fmaxf(2.0f * p.reflect - xn_main, 0.0f);
     return true;
   }
-  if (L.pend) {  // split the overshooting free step at the vertex (kernels.py:190-195)
-    float s = solve_bf(L.pa, L.pb, L.pc);
-    s = s < 0.0f ? 1.0f : s;
-    L.dtr = fmaxf((1.0f - s * s) * L.dtr, 0.0f);
+  if (L.pend) {
+    L.dtr = fmaxf(L.template split_factor<TAB>(G) * L.dtr, 0.0f);
     L.sq = fast_sqrt(L.dtr);
     L.pend = false;
   }
@@ -311,7 +315,7 @@ __device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph
   const float mu0 = L.template drift<TAB>(G, 0.0f);
   const float xn = fmaf(L.sig * L.sq, w, mu0 * L.dtr);
   if (xn >= 0.0f) {
-    L.x = (p.reflect > 0.0f && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
+    L.x = (REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
     return true;
   }
   const float alpha = (w * w * L.sig * L.sig) * fast_rcp(mu0 * mu0 * L.dtr);
@@ -334,9 +338,7 @@ __device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeG
                                              const Tables<SMEM> &T, const NatParams &p,
                                              float z, uint32_t u) {
   if (L.pend) {
-    float s = solve_bf(L.pa, L.pb, L.pc);
-    s = s < 0.0f ? 1.0f : s;
-    L.dtr = (1.0f - s * s) * L.dtr;
+    L.dtr = L.template split_factor<TAB>(G) * L.dtr;
     L.pend = false;
     if (L.dtr <= 0.0f) return true;  // step ends at the vertex, on the old edge
     if (L.M >= p.cap) {
@@ -350,27 +352,25 @@ __device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeG
   L.load_edge(T, s & 0x7fffffff, p.sqdt, 0.0f);
   L.x = s < 0 ? L.len : 0.0f;
   const float mu = L.template drift<TAB>(G, L.x);
-  const float a = mu * L.dtr;
-  const float b = (L.sig * L.sq) * z;
-  const float xn = L.x + a + b;
+  const float xn = fmaf(L.sig * L.sq, z, fmaf(mu, L.dtr, L.x));
   if (xn > 0.0f && xn < L.len) {
     L.x = xn;
     return true;
   }
   L.M += 1;
-  if (xn <= 0.0f)
-    L.set_hit(a, b, L.x, 0.0f);
-  else
-    L.set_hit(-a, -b, L.len - L.x, L.len);
+  L.pend = true;
+  L.px = L.x;
+  L.pz = z;
+  L.x = xn <= 0.0f ? 0.0f : L.len;
   return false;
 }
 
-template <bool STAR, bool SMEM, bool TAB>
+template <bool STAR, bool SMEM, bool TAB, bool REFLECT>
 __device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
                                           const Tables<SMEM> &T, const NatParams &p, float z,
                                           uint32_t u, float xn_main) {
   if constexpr (STAR)
-    return rare_star<SMEM, TAB>(L, G, T, p, z, u, xn_main);
+    return rare_star<SMEM, TAB, REFLECT>(L, G, T, p, z, u, xn_main);
   else
     return rare_general<SMEM, TAB>(L, G, T, p, z, u);
 }
@@ -378,40 +378,34 @@ __device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph
 // One trip for every lane of the warp.  `live` lanes advance; returns true for
 // lanes whose macro step completed.
 //
-// Common path: a lane strictly inside its edge always starts a fresh macro
+// Common path: a lane strictly inside its edge always begins a fresh macro
 // step (dtr == dt), so the proposal uses cached constants.  Accepted: done.
-// Overshoot at an end: the hit is recorded (x = vertex, quadratic saved) with
-// predicated moves; its split time is solved by the next (vertex) trip, so
-// all vertex work is one divergent region per trip.
-template <bool STAR, bool SMEM, bool TAB>
+// Overshoot at an end: the hit is recorded with predicated moves (x = the
+// vertex, start point and Gaussian saved) and its split time is solved by
+// the lane's next vertex trip, so all vertex work is one divergent region.
+// Lanes at a vertex run that region only on vertex slots (trip index a
+// multiple of rare_q; a function of the particle's own trip counter).
+template <bool STAR, bool SMEM, bool TAB, bool REFLECT>
 __device__ __forceinline__ bool trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
                                      const Tables<SMEM> &T, const Shared &S, const NatParams &p,
                                      bool live, bool vertex_slot, float z, uint32_t u) {
-  const float mu = L.template drift<TAB>(G, L.x);
-  const float a = mu * p.dt;
-  const float b = L.sig_sqdt * z;
-  const float xn = L.x + a + b;
-  const bool inside = STAR ? (L.x > 0.0f) : (L.x > 0.0f && L.x < L.len);
-  const bool lo_ok = xn > 0.0f, hi_ok = xn < L.len;
-  const bool run = live && inside;
-  const bool ok = run && lo_ok && hi_ok;
-  const bool hit_lo = run && !lo_ok;
-  const bool hit_hi = !STAR && run && lo_ok && !hi_ok;
-  if (hit_lo || hit_hi) {
+  const float xn = fmaf(L.sig_sqdt, z, fmaf(L.template drift<TAB>(G, L.x), p.dt, L.x));
+  const bool check_hi = !STAR || REFLECT;
+  const bool run = live && (L.x > 0.0f) && (STAR || L.x < L.len);
+  const bool lo_ok = xn > 0.0f;
+  const bool ok = run && lo_ok && (!check_hi || xn < L.len);
+  const bool hit = run && (STAR ? !lo_ok : !ok);
+  if (hit) {
     if (!STAR) L.M += 1;  // general counts hits; star counts vertex iterations
     L.pend = true;
-    L.pa = hit_lo ? a : -a;
-    L.pb = hit_lo ? b : -b;
-    L.pc = hit_lo ? L.x : L.len - L.x;
-    L.x = hit_lo ? 0.0f : L.len;
+    L.px = L.x;
+    L.pz = z;
+    L.x = (STAR || !lo_ok) ? 0.0f : L.len;
   }
-  L.x = ok ? xn : L.x;
+  if (ok) L.x = xn;
   bool done = ok;
-  // lanes at a vertex wait for their next vertex slot (deterministic per
-  // particle: slots depend only on the particle's own trip counter); a star
-  // proposal beyond the mirror wall is resolved at once
-  if (live && !ok && !(hit_lo || hit_hi) && (vertex_slot || (STAR && L.x > 0.0f))) {
-    done = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z, u, xn);
+  if (live && !ok && !hit && (vertex_slot || (REFLECT && L.x > 0.0f))) {
+    done = rare_trip<STAR, SMEM, TAB, REFLECT>(L, G, T, p, z, u, xn);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
   return done;
@@ -446,7 +440,7 @@ __device__ __forceinline__ void place_native(Lane<STAR, SMEM> &L, const NativeGr
   L.cross = L.events = L.truncs = 0;
 }
 
-template <bool STAR, bool SMEM, bool TAB>
+template <bool STAR, bool SMEM, bool TAB, bool REFLECT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o) {
   const int nb = p.cap + 1;
@@ -502,12 +496,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const Block r = native_block(p, pair++, kDomainEnsemble, id);
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
-    bool fin = false;
-    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active, (t0 & (q - 1)) == 0, z0, r.z))
-      fin = --L.steps_left == 0;
-    if (trip<STAR, SMEM, TAB>(L, G, T, S, p, active && !fin, ((t0 + 1) & (q - 1)) == 0, z1,
-                              r.w))
-      fin = --L.steps_left == 0;
+    L.steps_left -= trip<STAR, SMEM, TAB, REFLECT>(L, G, T, S, p, active,
+                                                   (t0 & (q - 1)) == 0, z0, r.z);
+    bool fin = L.steps_left == 0;
+    L.steps_left -= trip<STAR, SMEM, TAB, REFLECT>(L, G, T, S, p, active && !fin,
+                                                   ((t0 + 1) & (q - 1)) == 0, z1, r.w);
+    fin = fin || L.steps_left == 0;
     if (fin) finish();
   }
   if (o.totals) {
@@ -574,8 +568,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
     bool fin = false;
-    if (active) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z0, r.z, 0.0f);
-    if (active && !fin) fin = rare_trip<STAR, SMEM, TAB>(L, G, T, p, z1, r.w, 0.0f);
+    if (active) fin = rare_trip<STAR, SMEM, TAB, false>(L, G, T, p, z0, r.z, 0.0f);
+    if (active && !fin) fin = rare_trip<STAR, SMEM, TAB, false>(L, G, T, p, z1, r.w, 0.0f);
     if (fin) finish();
   }
   if (o.totals) {
@@ -709,9 +703,14 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   const size_t smem = smem_bytes(g, a.cap + 1, stage, false);
   const int d = g->device;
   const int64_t n = a.n_particles;
+  if (g->is_star && p.reflect > 0.0f)
+    return dispatch3(true, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
+      return launch(native_ensemble_kernel<true, decltype(sm)::value, decltype(tab)::value, true>,
+                    smem, d, n, s, g->nat, p, o);
+    });
   return dispatch3(g->is_star, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
     return launch(native_ensemble_kernel<decltype(star)::value, decltype(sm)::value,
-                                         decltype(tab)::value>,
+                                         decltype(tab)::value, false>,
                   smem, d, n, s, g->nat, p, o);
   });
 }
