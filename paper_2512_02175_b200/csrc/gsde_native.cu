@@ -498,10 +498,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     box_muller(r.x, r.y, z0, z1);
     L.steps_left -= trip<STAR, SMEM, TAB, REFLECT>(L, G, T, S, p, active,
                                                    (t0 & (q - 1)) == 0, z0, r.z);
-    bool fin = L.steps_left == 0;
+    bool fin = active && L.steps_left == 0;
     L.steps_left -= trip<STAR, SMEM, TAB, REFLECT>(L, G, T, S, p, active && !fin,
                                                    ((t0 + 1) & (q - 1)) == 0, z1, r.w);
-    fin = fin || L.steps_left == 0;
+    fin = active && L.steps_left == 0;
     if (fin) finish();
   }
   if (o.totals) {
