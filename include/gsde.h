@@ -114,6 +114,13 @@ typedef struct {
   const int64_t *hist_counts;  /* device [E]    (EdgeGrid.counts) */
   const double *hist_dx;       /* device [E]    (EdgeGrid.dx) */
   int64_t hist_n_cells;
+  /* Time-integrated occupation histogram on the same grid: after every
+   * occ_every-th completed macro step beyond step occ_start, each particle's
+   * (edge, x) is binned into occ (accumulated).  Requires the hist grid
+   * arrays; occ may be used with hist == NULL. */
+  int64_t *occ;                /* [n_cells] */
+  int64_t occ_every;           /* >= 1 */
+  int64_t occ_start;           /* steps before the first sample (burn-in) */
 } gsde_out;
 
 /* run_ensemble's kernel call: kernels.ensemble_star / ensemble_general

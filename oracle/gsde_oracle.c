@@ -136,6 +136,9 @@ double orc_u64_to_normal(uint64_t r) {
   return norm_ppf_qt(q, pt);
 }
 
+void orc_histogram(int64_t n, const int64_t *edges, const double *x, const int64_t *offsets,
+                   const int64_t *counts, const double *dx, int64_t *hist);
+
 /* ---- draw lookahead buffer (kernels.py:46, :55-64): value-neutral ---------- */
 #define ORC_BUF 64
 typedef struct {
@@ -428,6 +431,55 @@ void orc_ensemble(const orc_graph *g, int32_t star, uint64_t seed, int64_t n_par
       if (out_events) out_events[i] = events;
       if (out_trunc) out_trunc[i] = truncs;
     }
+  }
+}
+
+/* Time-integrated occupation histogram (the
+ * reference only snapshots, analysis.py:61-79): the ensemble loop of
+ * kernels.py:310-444 with (edge, x) binned exactly like histogram_accumulate
+ * after every `every`-th step beyond step `start`. */
+void orc_ensemble_occupation(const orc_graph *g, int32_t star, uint64_t seed,
+                             int64_t n_particles, int64_t pid_offset, int64_t n_steps, double dt,
+                             int32_t init_kind, int64_t init_edge, double init_x,
+                             double init_xmax, int64_t cap, double reflect_len,
+                             const int64_t *offsets, const int64_t *counts, const double *dx,
+                             int64_t every, int64_t start, int64_t *occ, int32_t n_threads) {
+  int64_t n_cells = offsets[g->n_edges];
+  int64_t n_chunks = (n_particles + ORC_CHUNK - 1) / ORC_CHUNK;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel
+#endif
+  {
+    int64_t *loc = calloc((size_t)n_cells, sizeof(int64_t));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      int64_t lo = c * ORC_CHUNK, hi = lo + ORC_CHUNK;
+      if (hi > n_particles) hi = n_particles;
+      for (int64_t i = lo; i < hi; ++i) {
+        uint64_t pid = (uint64_t)(i + pid_offset);
+        int64_t edge;
+        double x;
+        uint64_t k;
+        place(g, seed, pid, init_kind, init_edge, init_x, init_xmax, &edge, &x, &k);
+        orc_draws d;
+        draws_init(&d, seed, pid, k);
+        for (int64_t s = 0; s < n_steps; ++s) {
+          orc_step_out o = star ? step_star(g, edge, x, dt, &d, cap, reflect_len)
+                                : step_general(g, edge, x, dt, &d, cap);
+          edge = o.edge; x = o.x;
+          int64_t kk = s + 1 - start;
+          if (kk > 0 && kk % every == 0) orc_histogram(1, &edge, &x, offsets, counts, dx, loc);
+        }
+      }
+    }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+    for (int64_t j = 0; j < n_cells; ++j) occ[j] += loc[j];
+    free(loc);
   }
 }
 

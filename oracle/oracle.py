@@ -64,6 +64,9 @@ def lib():
                                         i64, P, P, P, P, i32]
         L.orc_histogram.argtypes = [i64, P, P, P, P, P, P]
         L.orc_max_threads.restype = C.c_int
+        L.orc_ensemble_occupation.argtypes = [C.POINTER(_Graph), i32, u64, i64, i64, i64, f64,
+                                              i32, i64, f64, f64, i64, f64, P, P, P, i64, i64,
+                                              P, i32]
         L.orc_fill_draws.argtypes = [u64, u64, i64, u64, i64, P, P, i32]
         L.orc_fill_draws_rows.argtypes = [P, P, P, i64, i64, P, P]
         _lib = L
@@ -204,3 +207,20 @@ def fill_draws_rows(seeds, pids, k0s, K):
     nrm = np.zeros((n, K), np.float64)
     lib().orc_fill_draws_rows(_ptr(seeds), _ptr(pids), _ptr(k0s), n, K, _ptr(raw), _ptr(nrm))
     return raw, nrm
+
+
+def ensemble_occupation(og: OracleGraph, seed, n, n_steps, dt, offsets, counts, dx, every=1,
+                        start=0, init=(0, 0, 0.0, 0.0), cap=100, reflect_len=0.0, pid_offset=0,
+                        threads=0):
+    """Time-integrated occupation histogram (samples after every ``every``-th
+    step beyond ``start``), reference streams."""
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    counts = np.ascontiguousarray(counts, np.int64)
+    dx = np.ascontiguousarray(dx, np.float64)
+    occ = np.zeros(int(counts.sum()), np.int64)
+    init_kind, init_edge, init_x, init_xmax = init
+    lib().orc_ensemble_occupation(C.byref(og.c), int(og.is_star), seed, n, pid_offset, n_steps,
+                                  dt, init_kind, init_edge, init_x, init_xmax, cap, reflect_len,
+                                  _ptr(offsets), _ptr(counts), _ptr(dx), every, start, _ptr(occ),
+                                  threads)
+    return occ

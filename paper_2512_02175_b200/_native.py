@@ -64,6 +64,7 @@ class Out(C.Structure):
         ("edge", _P), ("crossings", _P), ("events", _P), ("truncs", _P), ("x", _P),
         ("m_hist", _P), ("totals", _P), ("edge_counts", _P), ("hist", _P),
         ("hist_offsets", _P), ("hist_counts", _P), ("hist_dx", _P), ("hist_n_cells", _i64),
+        ("occ", _P), ("occ_every", _i64), ("occ_start", _i64),
     ]
 
 

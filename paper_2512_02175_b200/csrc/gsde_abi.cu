@@ -327,8 +327,12 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
     return set_error(GSDE_EINVAL, "ensemble: bad init_kind %d", a->init_kind);
   if (a->init_kind == GSDE_INIT_POINT && (a->init_edge < 0 || a->init_edge >= g->E))
     return set_error(GSDE_EINVAL, "ensemble: init_edge out of range");
-  if (o->hist && (!o->hist_offsets || !o->hist_counts || !o->hist_dx))
-    return set_error(GSDE_EINVAL, "ensemble: hist needs offsets, counts and dx");
+  if ((o->hist || o->occ) && (!o->hist_offsets || !o->hist_counts || !o->hist_dx ||
+                               o->hist_n_cells < 1))
+    return set_error(GSDE_EINVAL, "ensemble: hist/occ need offsets, counts, dx and n_cells");
+  if (o->occ && (o->occ_every < 1 || o->occ_start < 0 || o->occ_every > 0x7fffffff ||
+                 o->occ_start > 0x7fffffff))
+    return set_error(GSDE_EINVAL, "ensemble: occ_every must be >= 1 and occ_start >= 0");
   int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
                              "ensemble");
   if (rc) return rc;

@@ -155,12 +155,33 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
   return G.tab_mu[j - 1] + t * (G.tab_mu[j] - G.tab_mu[j - 1]);
 }
 
-// Shared block state: lane-private M counters, M histogram, totals, staged graph.
+// Compile-time kernel variant.
+template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_>
+struct Cfg {
+  static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
+  static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
+  static constexpr bool TAB = TAB_;          // some edge has a tabulated drift
+  static constexpr bool REFLECT = REFLECT_;  // star mirror wall enabled
+  static constexpr bool OCC = OCC_;          // time-integrated occupation histogram
+};
+
+// Occupation histogram: grid arrays + counters (shared uint32 or global int64).
+struct Occ {
+  const int64_t *off, *cnt;
+  const double *dx;
+  int64_t *out;
+  unsigned *s_cnt;   // shared counters, or null -> global atomics
+  int32_t every, start;
+};
+
+// Shared block state: lane-private M counters, M histogram, totals, staged
+// graph, occupation counters.
 struct Shared {
   int *priv;                 // [kPriv][kThreads]
   int *mh;                   // [cap+1]
   unsigned long long *tot;   // [4]
   int *exit_priv;            // trials: [E][kThreads] or null
+  unsigned *occ;             // [n_cells] or null
 };
 
 __device__ __forceinline__ size_t shared_head_bytes(int nb) {
@@ -169,7 +190,7 @@ __device__ __forceinline__ size_t shared_head_bytes(int nb) {
 
 template <bool STAR, bool SMEM>
 __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, Shared &S,
-                                             Tables<SMEM> &T, bool exit_priv) {
+                                             Tables<SMEM> &T, bool exit_priv, int occ_cells) {
   extern __shared__ __align__(16) unsigned char smem[];
   S.priv = reinterpret_cast<int *>(smem);
   S.mh = S.priv + kPriv * kThreads;
@@ -200,7 +221,13 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, Share
   S.exit_priv = nullptr;
   if (exit_priv) {
     S.exit_priv = reinterpret_cast<int *>(smem + off);
+    off += (size_t)G.n_edges * kThreads * sizeof(int);
     for (int j = threadIdx.x; j < G.n_edges * kThreads; j += blockDim.x) S.exit_priv[j] = 0;
+  }
+  S.occ = nullptr;
+  if (occ_cells > 0) {
+    S.occ = reinterpret_cast<unsigned *>(smem + off);
+    for (int j = threadIdx.x; j < occ_cells; j += blockDim.x) S.occ[j] = 0u;
   }
   __syncthreads();
 }
@@ -212,8 +239,8 @@ __device__ __forceinline__ void mh_add(const Shared &S, int bin) {
     atomicAdd(&S.mh[bin], 1);
 }
 
-__device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int64_t *totals,
-                             int n_tot) {
+__device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int occ_cells,
+                             int64_t *occ_out) {
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     int64_t v = S.mh[b];
@@ -221,12 +248,13 @@ __device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int64_t *
       for (int t = 0; t < kThreads; ++t) v += S.priv[b * kThreads + t];
     if (v && m_hist) add_i64(&m_hist[b], v);
   }
-  if (totals && threadIdx.x < n_tot && S.tot[threadIdx.x])
-    add_i64(&totals[threadIdx.x], (int64_t)S.tot[threadIdx.x]);
+  if (S.occ)
+    for (int j = threadIdx.x; j < occ_cells; j += blockDim.x)
+      if (S.occ[j]) add_i64(&occ_out[j], (int64_t)S.occ[j]);
 }
 
 // Per-lane simulation state.
-template <bool STAR, bool SMEM>
+template <class C>
 struct Lane {
   int e;           // current edge
   float x;         // position on e
@@ -240,37 +268,43 @@ struct Lane {
   int4 ev;         // endpoint alias info of e (general graphs)
   int steps_left;
   int cross, events, truncs;
+  int occ_left;    // steps to the next occupation sample
+  int occ_off, occ_top;  // grid cells of e: first index, count - 1
+  float occ_inv;   // 1 / cell width of e
 
-  __device__ __forceinline__ void load_edge(const Tables<SMEM> &T, int e2, float sqdt,
-                                            float star_len) {
+  __device__ __forceinline__ void load_edge(const Tables<C::SMEM> &T, const Occ &O, int e2,
+                                            float sqdt, float star_len) {
     const float4 r = T.E(e2);
     e = e2;
     mu_a = r.y;
     mu_b = r.z;
     sig = r.w;
     sig_sqdt = r.w * sqdt;
-    if (STAR) {
+    if (C::STAR) {
       len = star_len;
     } else {
       len = r.x;
       ev = T.V(e2);
     }
+    if (C::OCC) {
+      occ_off = (int)O.off[e2];
+      occ_top = (int)O.cnt[e2] - 1;
+      occ_inv = (float)(1.0 / O.dx[e2]);
+    }
   }
 
-  template <bool TAB>
   __device__ __forceinline__ float drift(const NativeGraph &G, float at) const {
-    if (TAB && isnan(mu_b)) return drift_tab(G, e, at);
+    if (C::TAB && isnan(mu_b)) return drift_tab(G, e, at);
     return fmaf(mu_b, at, mu_a);
   }
 
   // split time of the pending hit: the proposal x' = px + mu(px) dtr + sig sq pz
   // left the edge through the vertex the lane now sits at (kernels.py:190-195,
   // :276-283); residual time (1 - s^2) dtr
-  template <bool TAB>
   __device__ __forceinline__ float split_factor(const NativeGraph &G) const {
-    const float a = drift<TAB>(G, px) * dtr;
+    const float a = drift(G, px) * dtr;
     const float b = (sig * sq) * pz;
-    const bool lo = STAR || !(x > 0.0f);
+    const bool lo = C::STAR || !(x > 0.0f);
     float s = lo ? solve_bf(a, b, px) : solve_bf(-a, -b, len - px);
     s = s < 0.0f ? 1.0f : s;
     return 1.0f - s * s;
@@ -289,33 +323,47 @@ struct Lane {
     dtr = dt;
     sq = sqdt;
   }
+
+  // occupation sample of the state after a completed step (every `every` steps)
+  __device__ __forceinline__ void occ_tick(const Occ &O) {
+    if (--occ_left == 0) {
+      occ_left = O.every;
+      const int local = __float2int_rz(fminf(x * occ_inv, (float)occ_top));
+      const int cell = occ_off + (local < 0 ? 0 : local);
+      if (O.s_cnt)
+        atomicAdd(&O.s_cnt[cell], 1u);
+      else
+        add_i64(&O.out[cell], 1);
+    }
+  }
 };
 
 // Rare trip of a star graph (kernels.py:146-220).  Lanes arrive here at the
 // vertex (x == 0, possibly with an unresolved overshoot from an earlier trip)
 // or beyond the optional mirror wall.  Returns true when the macro step
 // completed.
-template <bool SMEM, bool TAB, bool REFLECT>
-__device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph &G,
-                                          const Tables<SMEM> &T, const NatParams &p, float z,
-                                          uint32_t u, float xn_main) {
-  if (REFLECT && L.x > 0.0f) {  // free step beyond the mirror wall (kernels.py:185-188)
+template <class C>
+__device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
+                                          const Tables<C::SMEM> &T, const Occ &O,
+                                          const NatParams &p, float z, uint32_t u,
+                                          float xn_main) {
+  if (C::REFLECT && L.x > 0.0f) {  // free step beyond the mirror wall (kernels.py:185-188)
     L.x = fmaxf(2.0f * p.reflect - xn_main, 0.0f);
     return true;
   }
   if (L.pend) {
-    L.dtr = fmaxf(L.template split_factor<TAB>(G) * L.dtr, 0.0f);
+    L.dtr = fmaxf(L.split_factor(G) * L.dtr, 0.0f);
     L.sq = fast_sqrt(L.dtr);
     L.pend = false;
   }
   // sample the exit edge, one-sided |W| excursion (kernels.py:198-220)
   L.M += 1;
-  L.load_edge(T, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
+  L.load_edge(T, O, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
   const float w = fabsf(z);
-  const float mu0 = L.template drift<TAB>(G, 0.0f);
+  const float mu0 = L.drift(G, 0.0f);
   const float xn = fmaf(L.sig * L.sq, w, mu0 * L.dtr);
   if (xn >= 0.0f) {
-    L.x = (REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
+    L.x = (C::REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
     return true;
   }
   const float alpha = (w * w * L.sig * L.sig) * fast_rcp(mu0 * mu0 * L.dtr);
@@ -333,12 +381,12 @@ __device__ __forceinline__ bool rare_star(Lane<true, SMEM> &L, const NativeGraph
 // Rare trip of a general graph (kernels.py:223-288).  Lanes arrive here at a
 // vertex: first resolve a pending hit (residual time, stop / cap checks),
 // then resample the exit slot and propose from the new edge's endpoint.
-template <bool SMEM, bool TAB>
-__device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeGraph &G,
-                                             const Tables<SMEM> &T, const NatParams &p,
-                                             float z, uint32_t u) {
+template <class C>
+__device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
+                                             const Tables<C::SMEM> &T, const Occ &O,
+                                             const NatParams &p, float z, uint32_t u) {
   if (L.pend) {
-    L.dtr = L.template split_factor<TAB>(G) * L.dtr;
+    L.dtr = L.split_factor(G) * L.dtr;
     L.pend = false;
     if (L.dtr <= 0.0f) return true;  // step ends at the vertex, on the old edge
     if (L.M >= p.cap) {
@@ -349,9 +397,9 @@ __device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeG
   }
   const bool at_init = !(L.x > 0.0f);
   const int s = alias_pick(T, at_init ? L.ev.x : L.ev.z, at_init ? L.ev.y : L.ev.w, u);
-  L.load_edge(T, s & 0x7fffffff, p.sqdt, 0.0f);
+  L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
   L.x = s < 0 ? L.len : 0.0f;
-  const float mu = L.template drift<TAB>(G, L.x);
+  const float mu = L.drift(G, L.x);
   const float xn = fmaf(L.sig * L.sq, z, fmaf(mu, L.dtr, L.x));
   if (xn > 0.0f && xn < L.len) {
     L.x = xn;
@@ -365,14 +413,15 @@ __device__ __forceinline__ bool rare_general(Lane<false, SMEM> &L, const NativeG
   return false;
 }
 
-template <bool STAR, bool SMEM, bool TAB, bool REFLECT>
-__device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
-                                          const Tables<SMEM> &T, const NatParams &p, float z,
-                                          uint32_t u, float xn_main) {
-  if constexpr (STAR)
-    return rare_star<SMEM, TAB, REFLECT>(L, G, T, p, z, u, xn_main);
+template <class C>
+__device__ __forceinline__ bool rare_trip(Lane<C> &L, const NativeGraph &G,
+                                          const Tables<C::SMEM> &T, const Occ &O,
+                                          const NatParams &p, float z, uint32_t u,
+                                          float xn_main) {
+  if constexpr (C::STAR)
+    return rare_star<C>(L, G, T, O, p, z, u, xn_main);
   else
-    return rare_general<SMEM, TAB>(L, G, T, p, z, u);
+    return rare_general<C>(L, G, T, O, p, z, u);
 }
 
 // One trip for every lane of the warp.  `live` lanes advance; returns true for
@@ -385,36 +434,38 @@ __device__ __forceinline__ bool rare_trip(Lane<STAR, SMEM> &L, const NativeGraph
 // the lane's next vertex trip, so all vertex work is one divergent region.
 // Lanes at a vertex run that region only on vertex slots (trip index a
 // multiple of rare_q; a function of the particle's own trip counter).
-template <bool STAR, bool SMEM, bool TAB, bool REFLECT>
-__device__ __forceinline__ bool trip(Lane<STAR, SMEM> &L, const NativeGraph &G,
-                                     const Tables<SMEM> &T, const Shared &S, const NatParams &p,
-                                     bool live, bool vertex_slot, float z, uint32_t u) {
-  const float xn = fmaf(L.sig_sqdt, z, fmaf(L.template drift<TAB>(G, L.x), p.dt, L.x));
-  const bool check_hi = !STAR || REFLECT;
-  const bool run = live && (L.x > 0.0f) && (STAR || L.x < L.len);
+template <class C>
+__device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
+                                     const Tables<C::SMEM> &T, const Shared &S, const Occ &O,
+                                     const NatParams &p, bool live, bool vertex_slot, float z,
+                                     uint32_t u) {
+  const float xn = fmaf(L.sig_sqdt, z, fmaf(L.drift(G, L.x), p.dt, L.x));
+  const bool check_hi = !C::STAR || C::REFLECT;
+  const bool run = live && (L.x > 0.0f) && (C::STAR || L.x < L.len);
   const bool lo_ok = xn > 0.0f;
   const bool ok = run && lo_ok && (!check_hi || xn < L.len);
-  const bool hit = run && (STAR ? !lo_ok : !ok);
+  const bool hit = run && (C::STAR ? !lo_ok : !ok);
   if (hit) {
-    if (!STAR) L.M += 1;  // general counts hits; star counts vertex iterations
+    if (!C::STAR) L.M += 1;  // general counts hits; star counts vertex iterations
     L.pend = true;
     L.px = L.x;
     L.pz = z;
-    L.x = (STAR || !lo_ok) ? 0.0f : L.len;
+    L.x = (C::STAR || !lo_ok) ? 0.0f : L.len;
   }
   if (ok) L.x = xn;
   bool done = ok;
-  if (live && !ok && !hit && (vertex_slot || (REFLECT && L.x > 0.0f))) {
-    done = rare_trip<STAR, SMEM, TAB, REFLECT>(L, G, T, p, z, u, xn);
+  if (live && !ok && !hit && (vertex_slot || (C::REFLECT && L.x > 0.0f))) {
+    done = rare_trip<C>(L, G, T, O, p, z, u, xn);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
+  if (C::OCC && done) L.occ_tick(O);
   return done;
 }
 
-template <bool STAR, bool SMEM>
-__device__ __forceinline__ void place_native(Lane<STAR, SMEM> &L, const NativeGraph &G,
-                                             const Tables<SMEM> &T, const NatParams &p,
-                                             uint64_t id, float star_len) {
+template <class C>
+__device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
+                                             const Tables<C::SMEM> &T, const Occ &O,
+                                             const NatParams &p, uint64_t id, float star_len) {
   int e;
   float x;
   if (p.init_kind == GSDE_INIT_POINT) {
@@ -429,7 +480,7 @@ __device__ __forceinline__ void place_native(Lane<STAR, SMEM> &L, const NativeGr
     const double le = (double)T.E(e).x;
     x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
   }
-  L.load_edge(T, e, p.sqdt, star_len);
+  L.load_edge(T, O, e, p.sqdt, star_len);
   L.x = x;
   L.dtr = p.dt;
   L.sq = p.sqdt;
@@ -438,25 +489,29 @@ __device__ __forceinline__ void place_native(Lane<STAR, SMEM> &L, const NativeGr
   L.pend = false;
   L.steps_left = p.n_steps;
   L.cross = L.events = L.truncs = 0;
+  L.occ_left = O.start + O.every;
 }
 
-template <bool STAR, bool SMEM, bool TAB, bool REFLECT>
+template <class C>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
-    native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o) {
+    native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells) {
   const int nb = p.cap + 1;
   Shared S;
-  Tables<SMEM> T;
-  shared_setup<STAR, SMEM>(G, nb, S, T, false);
-  const float star_len = p.reflect > 0.0f ? p.reflect : __int_as_float(0x7f800000);
+  Tables<C::SMEM> T;
+  shared_setup<C::STAR, C::SMEM>(G, nb, S, T, false, C::OCC ? occ_smem_cells : 0);
+  Occ O{o.hist_offsets, o.hist_counts, o.hist_dx, o.occ, S.occ, (int32_t)o.occ_every,
+        (int32_t)o.occ_start};
+  const float star_len = C::REFLECT ? p.reflect : __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  Lane<STAR, SMEM> L;
+  Lane<C> L;
   L.x = 1.0f;
   L.len = star_len;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
   L.pend = false;
   L.M = 0;
   L.steps_left = 1;
+  L.occ_left = 1 << 30;
   uint32_t pair = 0;
   uint64_t id = 0;
   int64_t t_cross = 0, t_events = 0, t_truncs = 0;
@@ -479,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   if (p.n_steps == 0) {  // placement only (engine.py:329-336)
     while (waiting) {
       id = (uint64_t)(p.id_offset + i);
-      place_native(L, G, T, p, id, star_len);
+      place_native(L, G, T, O, p, id, star_len);
       finish();
     }
   }
@@ -487,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   for (uint32_t it = 0; __any_sync(0xffffffffu, active || waiting); ++it) {
     if (waiting && (it & (period - 1)) == 0) {
       id = (uint64_t)(p.id_offset + i);
-      place_native(L, G, T, p, id, star_len);
+      place_native(L, G, T, O, p, id, star_len);
       pair = 0;
       waiting = false;
       active = true;
@@ -496,11 +551,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const Block r = native_block(p, pair++, kDomainEnsemble, id);
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
-    L.steps_left -= trip<STAR, SMEM, TAB, REFLECT>(L, G, T, S, p, active,
-                                                   (t0 & (q - 1)) == 0, z0, r.z);
+    L.steps_left -= trip<C>(L, G, T, S, O, p, active, (t0 & (q - 1)) == 0, z0, r.z);
     bool fin = active && L.steps_left == 0;
-    L.steps_left -= trip<STAR, SMEM, TAB, REFLECT>(L, G, T, S, p, active && !fin,
-                                                   ((t0 + 1) & (q - 1)) == 0, z1, r.w);
+    L.steps_left -= trip<C>(L, G, T, S, O, p, active && !fin, ((t0 + 1) & (q - 1)) == 0, z1,
+                            r.w);
     fin = active && L.steps_left == 0;
     if (fin) finish();
   }
@@ -509,30 +563,31 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     warp_add_i64(&o.totals[1], t_events);
     warp_add_i64(&o.totals[2], t_truncs);
   }
-  shared_flush(S, nb, o.m_hist, nullptr, 0);
+  shared_flush(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
 }
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
 // fused exit counts per edge and M histogram including M = 0.
-template <bool STAR, bool SMEM, bool TAB>
+template <class C>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv) {
   const int nb = p.cap + 1;
   Shared S;
-  Tables<SMEM> T;
-  shared_setup<STAR, SMEM>(G, nb, S, T, exit_priv != 0);
+  Tables<C::SMEM> T;
+  shared_setup<C::STAR, C::SMEM>(G, nb, S, T, exit_priv != 0, 0);
+  const Occ O{};
   const float inf = __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool active = i < p.n;
-  Lane<STAR, SMEM> L;
+  Lane<C> L;
   uint32_t pair = 0;
   uint64_t id = 0;
   int64_t t_M = 0, t_ev = 0, t_tr = 0;
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
-    L.load_edge(T, STAR ? 0 : p.start_edge, p.sqdt, inf);
-    L.x = STAR ? 0.0f : p.start_x;
+    L.load_edge(T, O, C::STAR ? 0 : p.start_edge, p.sqdt, inf);
+    L.x = C::STAR ? 0.0f : p.start_x;
     L.dtr = p.dt;
     L.sq = p.sqdt;
     L.M = 0;
@@ -568,8 +623,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
     bool fin = false;
-    if (active) fin = rare_trip<STAR, SMEM, TAB, false>(L, G, T, p, z0, r.z, 0.0f);
-    if (active && !fin) fin = rare_trip<STAR, SMEM, TAB, false>(L, G, T, p, z1, r.w, 0.0f);
+    if (active) fin = rare_trip<C>(L, G, T, O, p, z0, r.z, 0.0f);
+    if (active && !fin) fin = rare_trip<C>(L, G, T, O, p, z1, r.w, 0.0f);
     if (fin) finish();
   }
   if (o.totals) {
@@ -577,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     warp_add_i64(&o.totals[1], t_ev);
     warp_add_i64(&o.totals[2], t_tr);
   }
-  shared_flush(S, nb, o.m_hist, nullptr, 0);
+  shared_flush(S, nb, o.m_hist, 0, nullptr);
   if (S.exit_priv && o.exit_counts) {
     for (int e = threadIdx.x; e < G.n_edges; e += blockDim.x) {
       int64_t v = 0;
@@ -615,11 +670,14 @@ __global__ void __launch_bounds__(256) histogram_kernel(int64_t n, const int64_t
   }
 }
 
-size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit) {
+constexpr int kOccSmemCells = 8192;  // shared uint32 occupation counters up to 32 KB
+
+size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit, int occ_cells) {
   size_t b = ((size_t)(kPriv * kThreads + nb) * sizeof(int) + 15) & ~size_t(15);
   b += 4 * sizeof(unsigned long long);
   if (stage) b += (size_t)g->E * (g->is_star ? 16 : 32) + (size_t)g->S * 16;
   if (priv_exit) b += (size_t)g->E * kThreads * sizeof(int);
+  b += (size_t)occ_cells * sizeof(unsigned);
   return b;
 }
 
@@ -663,28 +721,31 @@ NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t 
 }
 
 template <class K, class... Args>
-cudaError_t launch(K kernel, size_t smem, int device, int64_t n, cudaStream_t s, Args... args) {
-  if (smem > 48 * 1024) {
-    cudaError_t err =
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-  }
-  kernel<<<occupancy_grid(kernel, smem, device, n), kThreads, smem, s>>>(args...);
+cudaError_t launch(K kernel, size_t smem, int grid, cudaStream_t s, Args... args) {
+  kernel<<<grid, kThreads, smem, s>>>(args...);
   count_launch();
   return cudaGetLastError();
 }
 
-// Runtime flags -> compile-time kernel variant.
-template <class F>
-cudaError_t dispatch3(bool a, bool b, bool c, F &&f) {
+template <class K>
+cudaError_t prepare(K kernel, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// Runtime flags -> compile-time kernel variant (Cfg).
+template <bool OCC, class F>
+cudaError_t dispatch(bool star, bool smem, bool tab, bool reflect, F &&f) {
   using T = std::true_type;
   using N = std::false_type;
-  if (a) {
-    if (b) return c ? f(T{}, T{}, T{}) : f(T{}, T{}, N{});
-    return c ? f(T{}, N{}, T{}) : f(T{}, N{}, N{});
-  }
-  if (b) return c ? f(N{}, T{}, T{}) : f(N{}, T{}, N{});
-  return c ? f(N{}, N{}, T{}) : f(N{}, N{}, N{});
+  auto with = [&](auto st, auto sm) -> cudaError_t {
+    constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
+    if (ST && reflect)
+      return tab ? f(Cfg<ST, SM, true, true, OCC>{}) : f(Cfg<ST, SM, false, true, OCC>{});
+    return tab ? f(Cfg<ST, SM, true, false, OCC>{}) : f(Cfg<ST, SM, false, false, OCC>{});
+  };
+  if (star) return smem ? with(T{}, T{}) : with(T{}, N{});
+  return smem ? with(N{}, T{}) : with(N{}, N{});
 }
 
 }  // namespace
@@ -700,19 +761,30 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   p.init_xmax = a.init_xmax;
   p.rare_q = rare_period();
   const bool stage = g->nat_graph_smem > 0;
-  const size_t smem = smem_bytes(g, a.cap + 1, stage, false);
+  const bool occ = o.occ != nullptr;
   const int d = g->device;
   const int64_t n = a.n_particles;
-  if (g->is_star && p.reflect > 0.0f)
-    return dispatch3(true, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
-      return launch(native_ensemble_kernel<true, decltype(sm)::value, decltype(tab)::value, true>,
-                    smem, d, n, s, g->nat, p, o);
-    });
-  return dispatch3(g->is_star, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
-    return launch(native_ensemble_kernel<decltype(star)::value, decltype(sm)::value,
-                                         decltype(tab)::value, false>,
-                  smem, d, n, s, g->nat, p, o);
-  });
+  auto run = [&](auto cfg) -> cudaError_t {
+    using C = decltype(cfg);
+    auto k = native_ensemble_kernel<C>;
+    // occupation counters in shared memory when the grid is small and no
+    // per-block count can overflow 32 bits
+    int occ_cells = 0;
+    if (C::OCC && o.hist_n_cells <= kOccSmemCells) occ_cells = (int)o.hist_n_cells;
+    size_t smem = smem_bytes(g, a.cap + 1, stage, false, occ_cells);
+    cudaError_t err = prepare(k, smem);
+    if (err != cudaSuccess) return err;
+    const int grid = occupancy_grid(k, smem, d, n);
+    if (occ_cells) {
+      const double per_block = (double)((n + grid - 1) / grid) *
+                               ((double)a.n_steps / (double)(o.occ_every > 0 ? o.occ_every : 1));
+      if (per_block >= 4.0e9) occ_cells = 0;
+    }
+    smem = smem_bytes(g, a.cap + 1, stage, false, occ_cells);
+    return launch(k, smem, grid, s, g->nat, p, o, occ_cells);
+  };
+  return occ ? dispatch<true>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run)
+             : dispatch<false>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
@@ -722,13 +794,14 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   p.start_x = (float)a.start_x;
   const int priv = (o.exit_counts && g->E <= 32) ? 1 : 0;
   const bool stage = g->nat_graph_smem > 0;
-  const size_t smem = smem_bytes(g, a.cap + 1, stage, priv);
+  const size_t smem = smem_bytes(g, a.cap + 1, stage, priv, 0);
   const int d = g->device;
   const int64_t n = a.n_trials;
-  return dispatch3(g->is_star, stage, g->has_tab, [&](auto star, auto sm, auto tab) {
-    return launch(native_trials_kernel<decltype(star)::value, decltype(sm)::value,
-                                       decltype(tab)::value>,
-                  smem, d, n, s, g->nat, p, o, priv);
+  return dispatch<false>(g->is_star, stage, g->has_tab, false, [&](auto cfg) -> cudaError_t {
+    auto k = native_trials_kernel<decltype(cfg)>;
+    cudaError_t err = prepare(k, smem);
+    if (err != cudaSuccess) return err;
+    return launch(k, smem, occupancy_grid(k, smem, d, n), s, g->nat, p, o, priv);
   });
 }
 

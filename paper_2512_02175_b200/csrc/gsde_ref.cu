@@ -262,6 +262,11 @@ __global__ void __launch_bounds__(256) ref_ensemble_kernel(RefGraph<R> g, gsde_r
           add_i64(&o.m_hist[mm], 1);
         if (so.trunc) truncs += 1;
       }
+      if (o.occ) {  // time-integrated occupation: sample after selected steps
+        const int64_t k = s + 1 - o.occ_start;
+        if (k > 0 && k % o.occ_every == 0)
+          add_i64(&o.occ[hist_cell(o.hist_offsets, o.hist_counts, o.hist_dx, edge, (double)x)], 1);
+      }
     }
     t_over += d.overrun() ? 1 : 0;
     t_cross += cross;

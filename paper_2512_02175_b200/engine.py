@@ -195,7 +195,7 @@ def _check_ensemble_shape(graph: MetricGraph, config: SimulationConfig) -> None:
 
 
 def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, outputs=("all",),
-                    grid=None, inject=None, precision="f32", stream=None):
+                    grid=None, inject=None, precision="f32", stream=None, occupation=None):
     """Run an ensemble and return DEVICE tensors (no host copies).
 
     ``outputs``: any of ``"edge", "x", "crossings", "events", "truncs"`` or
@@ -204,7 +204,10 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
     (an :class:`EdgeGrid`) is given.  ``pid_offset`` / ``n_particles`` select
     a shard of global particle ids (multi-GPU).  ``inject=(raw, normal)``
     (device uint64 / float64 tensors ``[n, K]``) selects the injected-draw
-    stream with ``precision`` ``"f32"`` or ``"f64"``.
+    stream with ``precision`` ``"f32"`` or ``"f64"``.  ``occupation=(every,
+    start)`` (needs ``grid``) adds the time-integrated occupation histogram
+    ``res["occ"]``: every particle's (edge, x) binned after every
+    ``every``-th completed macro step beyond step ``start``.
     """
     torch, dev = _native.torch_cuda(config.device)
     n = config.n_particles if n_particles is None else int(n_particles)
@@ -234,15 +237,23 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
                  ("truncs", tr_t), ("m_hist", res["m_hist"]), ("totals", res["totals"]),
                  ("edge_counts", ec_t)):
         setattr(o, k, _native.ptr(t))
+    if occupation is not None and grid is None:
+        raise ConfigInvalid("the occupation histogram needs a grid")
     if grid is not None:
         res["hist"] = torch.zeros(grid.n_cells, dtype=torch.int64, **kw)
-        g_off = torch.as_tensor(grid.offsets, **kw)
-        g_cnt = torch.as_tensor(grid.counts, **kw)
-        g_dx = torch.as_tensor(grid.dx, **kw)
+        g_off = torch.tensor(grid.offsets, **kw)
+        g_cnt = torch.tensor(grid.counts, **kw)
+        g_dx = torch.tensor(grid.dx, **kw)
         res["_grid"] = (g_off, g_cnt, g_dx)
         o.hist, o.hist_offsets, o.hist_counts, o.hist_dx = (
             res["hist"].data_ptr(), g_off.data_ptr(), g_cnt.data_ptr(), g_dx.data_ptr())
         o.hist_n_cells = grid.n_cells
+        if occupation is not None:
+            every, start = (int(v) for v in occupation)
+            if every < 1 or start < 0:
+                raise ConfigInvalid("occupation needs every >= 1 and start >= 0")
+            res["occ"] = torch.zeros(grid.n_cells, dtype=torch.int64, **kw)
+            o.occ, o.occ_every, o.occ_start = res["occ"].data_ptr(), every, start
     init_kind, init_edge, init_x, init_xmax = _resolve_initial(graph, config.initial)
     r = _native.Run()
     r.seed = int(config.seed) & 0xFFFFFFFFFFFFFFFF

@@ -239,3 +239,41 @@ def test_edge_cases():
                                                   seed=5, reflect_at=0.05,
                                                   initial=gs.PerEdgeUniform(0.05)))
     assert np.all(r.positions <= 0.05)
+
+
+def test_occupation_native_vs_reference_and_invariants():
+    g, f = workloads.hub64()
+    grid = gs.EdgeGrid.uniform(g, 8)
+    mk = lambda rng, s: gs.SimulationConfig(dt=1e-3, n_steps=400, n_particles=200_000, seed=s,
+                                            initial=gs.PerEdgeUniform(2.0), rng=rng)
+    hn, sn = analysis.run_ensemble_occupation(g, f, mk("native", 1), grid, every=4, start=100)
+    hr, sr = analysis.run_ensemble_occupation(g, f, mk("reference", 2), grid, every=4, start=100)
+    assert hn.counts.sum() == hn.total == 200_000 * 75
+    assert hr.counts.sum() == hr.total
+    # time-correlated samples: compare occupation of each edge (coarse) with a
+    # loose chi-square (samples of one particle are correlated)
+    pn = hn.counts.reshape(64, 8).sum(1) / hn.total
+    pr = hr.counts.reshape(64, 8).sum(1) / hr.total
+    assert np.max(np.abs(pn - pr)) < 0.003, np.max(np.abs(pn - pr))
+    # big grid: global-atomic path gives the same totals
+    big = gs.EdgeGrid.uniform(g, 200)
+    hb, _ = analysis.run_ensemble_occupation(g, f, mk("native", 1), big, every=4, start=100)
+    assert hb.counts.sum() == hb.total
+    np.testing.assert_array_equal(hb.counts.reshape(64, 200).sum(1), hn.counts.reshape(64, 8).sum(1))
+
+
+@pytest.mark.parametrize("kind", ["linear", "quadratic"])
+def test_occupation_density_beats_snapshot_l2(kind):
+    """Time-averaged occupation after burn-in: the §4.1 steady state from 1e5
+    particles, compared with the snapshot estimator at the same N."""
+    g, f = workloads.star5(kind)
+    oracle_ = analysis.SteadyStateOracle.from_field(g, f)
+    grid = gs.EdgeGrid.uniform(g, 200, lengths=oracle_.truncation_lengths(1e-8))
+    cfg = gs.SimulationConfig(dt=1e-4, n_steps=20_000, n_particles=100_000, seed=9)
+    ho, _ = analysis.run_ensemble_occupation(g, f, cfg, grid, every=10, start=5_000)
+    hs, _ = analysis.run_ensemble_histogram(g, f, cfg, grid)
+    eo, es = analysis.l2_error(ho, oracle_), analysis.l2_error(hs, oracle_)
+    print(f"{kind}: occupation L2 {eo:.4f}, snapshot L2 {es:.4f}")
+    assert eo < es
+    if kind == "quadratic":
+        assert eo < 0.05

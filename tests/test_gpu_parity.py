@@ -243,3 +243,23 @@ def test_sharded_reference_run_equals_single_run():
     for k in ("edge", "x", "crossings"):
         assert torch.equal(full[k], torch.cat([p[k] for p in parts])), k
     assert torch.equal(full["m_hist"], parts[0]["m_hist"] + parts[1]["m_hist"])
+
+
+@pytest.mark.parametrize("case,every,start,init", [
+    ("star5_quad", 1, 0, ("at", 0)),
+    ("hub8", 3, 7, ("uniform", 2.0)),
+    ("random_general", 5, 0, ("uniform", 1.0)),
+])
+def test_occupation_reference_stream_matches_oracle(case, every, start, init):
+    """Time-integrated occupation (§8(f) rank 1), reference stream: exact."""
+    g, f = helpers.graph_for(case)
+    lengths = None if not g.has_semi_infinite_edges else [0.3] * g.n_edges
+    grid = gs.EdgeGrid.uniform(g, 6, lengths=lengths)
+    cfg = gs.SimulationConfig(dt=2e-3, n_steps=60, n_particles=3000, seed=31,
+                              initial=helpers.initial_for(init), rng="reference")
+    h, _ = analysis.run_ensemble_occupation(g, f, cfg, grid, every=every, start=start)
+    occ = oracle.ensemble_occupation(oracle.OracleGraph(g, f), 31, 3000, 60, 2e-3, grid.offsets,
+                                     grid.counts, grid.dx, every, start,
+                                     helpers.oracle_init(init, g))
+    np.testing.assert_array_equal(h.counts, occ)
+    assert h.total == 3000 * ((60 - start) // every) == int(occ.sum())
