@@ -188,6 +188,22 @@ int gsde_histogram(int64_t n, const int64_t *edge, const double *x, const int64_
                    const int64_t *counts, const double *dx, int64_t n_cells, int64_t *hist,
                    void *stream);
 
+/* Native reader for the "metric-graph v1" text format (graphfile.py:69-186),
+ * happy path only: returns GSDE_OK and an opaque result, or a nonzero code for
+ * any input it does not accept verbatim -- the caller then re-parses with the
+ * Python parser, which raises the reference's exact ParseError.  Host-only. */
+typedef struct gsde_parsed_s gsde_parsed;
+int gsde_parse_graph_text(const char *text, int64_t len, gsde_parsed **out);
+/* sizes[7]: vertex declarations, edges, weight directives, weight values,
+ * drift directives, tabulated samples, sigma directives */
+void gsde_parsed_sizes(const gsde_parsed *p, int64_t *sizes);
+void gsde_parsed_export(const gsde_parsed *p, int64_t *vdecl, int64_t *e_id, int64_t *e_init,
+                        int64_t *e_term, double *e_len, int64_t *w_vertex, int64_t *w_n,
+                        double *w_val, int64_t *d_id, int8_t *d_kind, double *d_a, double *d_b,
+                        int64_t *d_tab_n, double *tab_x, double *tab_mu, int64_t *s_id,
+                        double *s_val);
+void gsde_parsed_free(gsde_parsed *p);
+
 /* Host-side scalar helpers, compiled from the same sources as the kernels. */
 uint64_t gsde_raw64(uint64_t seed, uint64_t stream, uint64_t index); /* rng.py:45-66 */
 double gsde_uniform01(uint64_t seed, uint64_t stream, uint64_t index); /* rng.py:75-78 */

@@ -96,7 +96,8 @@ EXPORTS = (
     "gsde_graph_create", "gsde_graph_destroy", "gsde_graph_device_bytes", "gsde_ensemble",
     "gsde_vertex_trials", "gsde_step_batch", "gsde_histogram", "gsde_raw64", "gsde_uniform01",
     "gsde_normal", "gsde_solve_first_passage_s", "gsde_launch_count", "gsde_abi_version",
-    "gsde_last_error",
+    "gsde_last_error", "gsde_parse_graph_text", "gsde_parsed_sizes", "gsde_parsed_export",
+    "gsde_parsed_free",
 )
 
 _lib = None
@@ -130,6 +131,13 @@ def lib():
                     getattr(L, name).restype = _f64
                 L.gsde_solve_first_passage_s.argtypes = [_f64, _f64, _f64]
                 L.gsde_solve_first_passage_s.restype = _f64
+                L.gsde_parse_graph_text.argtypes = [C.c_char_p, _i64, C.POINTER(_P)]
+                L.gsde_parsed_sizes.argtypes = [_P, _P]
+                L.gsde_parsed_sizes.restype = None
+                L.gsde_parsed_export.argtypes = [_P] * 18
+                L.gsde_parsed_export.restype = None
+                L.gsde_parsed_free.argtypes = [_P]
+                L.gsde_parsed_free.restype = None
                 L.gsde_launch_count.restype = _i64
                 L.gsde_last_error.restype = C.c_char_p
                 assert L.gsde_abi_version() == 1, "libgsde ABI mismatch"

@@ -259,6 +259,30 @@ def build_graph(edges, jump_weights: dict | None = None) -> MetricGraph:
     WeightSimplexViolation, DisconnectedGraph.
     """
     init, term, length = _validate_edges(edges)
+    return build_graph_arrays(init, term, length, jump_weights)
+
+
+def _edges_valid(init: np.ndarray, term: np.ndarray, length: np.ndarray) -> bool:
+    """Vectorised form of the per-edge checks of :func:`_validate_edges`."""
+    inf_len = np.isinf(length)
+    return bool(
+        np.all(length > 0.0)
+        and np.array_equal(inf_len, term == INFINITY_VERTEX)
+        and np.all(init >= 0)
+        and np.all((term >= 0) | (term == INFINITY_VERTEX))
+        and not np.any(init == term)
+    )
+
+
+def build_graph_arrays(init, term, length, jump_weights: dict | None = None) -> MetricGraph:
+    """:func:`build_graph` from edge arrays (int64 init/term with -1 for the
+    vertex at infinity, float64 lengths).  Arrays that fail the per-edge
+    checks are re-validated edge by edge for the reference's error."""
+    init = np.ascontiguousarray(init, dtype=np.int64)
+    term = np.ascontiguousarray(term, dtype=np.int64)
+    length = np.ascontiguousarray(length, dtype=np.float64)
+    if not _edges_valid(init, term, length):
+        init, term, length = _validate_edges(zip(init.tolist(), term.tolist(), length.tolist()))
     m = int(init.shape[0])
     if m == 0:
         raise GraphBuildError("a metric graph needs at least one edge")

@@ -192,3 +192,56 @@ def test_workloads_deterministic():
     assert t1 == t2
     g, f = gs.parse_graph_file(t1)
     assert g.n_edges >= g.n_vertices - 1
+
+
+def _same_graph(a, b):
+    (g1, f1), (g2, f2) = a, b
+    for k in ("edge_init", "edge_term", "edge_length", "v_off", "v_edges", "v_orient", "v_cumw"):
+        np.testing.assert_array_equal(getattr(g1, k), getattr(g2, k), err_msg=k)
+    assert g1.is_star == g2.is_star
+    for x, y in zip(f1.packed(), f2.packed()):
+        np.testing.assert_array_equal(x, y)
+    assert f1.drift == f2.drift and f1.diffusion == f2.diffusion
+
+
+@pytest.mark.parametrize("case", list(cases.CASES) + ["vascular_small"])
+def test_native_graph_reader_matches_python_reader(case):
+    g, f = _built(case)
+    text = gs.serialize_graph_file(g, f)
+    fast = graphfile._parse_native(text)
+    assert fast is not None, "native reader should accept serialized files"
+    _same_graph(fast, graphfile._parse_python(text))
+
+
+BAD_DOCS = [
+    "",
+    "metric-graph  v1\nedge 0 0 1 1.0\n",                  # header spacing
+    "metric-graph v1\nedge 0 0 1\n",                         # arity
+    "metric-graph v1\nedge 0 0 1 1.0\nedge 0 1 2 1.0\n",     # duplicate id
+    "metric-graph v1\nedge 1 0 1 1.0\n",                     # ids not dense
+    "metric-graph v1\nedge 0 0 1 -1.0\n",                    # NonPositiveLength
+    "metric-graph v1\nedge 0 0 0 1.0\n",                     # self loop
+    "metric-graph v1\nedge 0 0 inf inf\nweights inf 1.0\n",  # weights at infinity
+    "metric-graph v1\nedge 0 0 1 1.0\ndrift 0 from_flux 1.0 0.0\n",
+    "metric-graph v1\nedge 0 0 1 1.0\ndrift 0 tabulated 0.5:1 0.2:3\n",
+    "metric-graph v1\nedge 0 0 1 1.0\ndrift 0 tabulated 0.5:1 2.0:3\n",  # beyond edge
+    "metric-graph v1\nedge 0 0 1 1.0\nsigma 0 0.0\n",        # ZeroDiffusion
+    "metric-graph v1\nvertex 0\nedge 0 0 1 1.0\n",           # undeclared vertex 1
+    "metric-graph v1\nedge 0 0 1 1.0\nweights 0 0.5 0.5\n",  # weight arity
+    "metric-graph v1\nedge 0 0 1 1.0\nfoo 1\n",              # unknown directive
+    "metric-graph v1\nedge 0 0 1 1_0.0\n",                   # python-only number syntax
+    "metric-graph v1\nedge 0 0 1 0x1p3\n",                   # hex float (python rejects)
+    "metric-graph v1\nedge 0 0 1 1.0\x0bedge 1 1 2 1.0\n",   # \v is a line break in python
+]
+
+
+@pytest.mark.parametrize("doc", BAD_DOCS)
+def test_reader_errors_and_fallbacks_are_the_python_readers(doc):
+    try:
+        want = graphfile._parse_python(doc)
+    except gs.ParseError as err:
+        with pytest.raises(gs.ParseError) as got:
+            gs.parse_graph_file(doc)
+        assert (got.value.line, str(got.value)) == (err.line, str(err))
+    else:
+        _same_graph(gs.parse_graph_file(doc), want)
