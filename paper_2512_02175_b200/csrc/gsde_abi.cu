@@ -90,6 +90,42 @@ void build_alias(const double *w, int deg, std::vector<double> &prob, std::vecto
   for (int j : large) prob[j] = 1.0, alias[j] = j;
 }
 
+// Recycled device arenas (graph handles are often re-created per call with
+// the same size): avoids cudaMalloc / cudaFree -- both device-synchronising
+// and slow once the process holds large caching-allocator pools.
+struct ArenaPool {
+  struct Entry {
+    int device;
+    void *ptr;
+    size_t bytes;
+  };
+  std::mutex mu;
+  std::vector<Entry> free;
+  void *take(int device, size_t bytes, size_t *got) {
+    std::lock_guard<std::mutex> lock(mu);
+    for (size_t i = 0; i < free.size(); ++i) {
+      const Entry e = free[i];
+      if (e.device == device && e.bytes >= bytes && e.bytes <= 2 * bytes + 4096) {
+        free.erase(free.begin() + (long)i);
+        *got = e.bytes;
+        return e.ptr;
+      }
+    }
+    return nullptr;
+  }
+  // returns false when the pool is full (caller frees)
+  bool give(int device, void *ptr, size_t bytes) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (free.size() >= 16) return false;
+    free.push_back(Entry{device, ptr, bytes});
+    return true;
+  }
+};
+ArenaPool &arena_pool() {
+  static ArenaPool *pool = new ArenaPool();  // never destroyed: outlives static teardown
+  return *pool;
+}
+
 struct Arena {
   std::vector<unsigned char> host;
   size_t add(const void *src, size_t bytes) {
@@ -236,10 +272,14 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
                o_nedge = A.add(nedge.data(), E * sizeof(float4)),
                o_nedgev = A.add(nedgev.data(), E * sizeof(int4)),
                o_ncol = A.add(ncol.data(), S * sizeof(int4));
-  void *dev = nullptr;
-  cudaError_t err = cudaMalloc(&dev, A.host.size());
-  if (err != cudaSuccess) return set_error(GSDE_ENOMEM, "graph_create: cudaMalloc(%zu): %s",
-                                           A.host.size(), cudaGetErrorString(err));
+  size_t arena_bytes = A.host.size();
+  void *dev = arena_pool().take(device, A.host.size(), &arena_bytes);
+  cudaError_t err = cudaSuccess;
+  if (!dev) {
+    err = cudaMalloc(&dev, A.host.size());
+    if (err != cudaSuccess) return set_error(GSDE_ENOMEM, "graph_create: cudaMalloc(%zu): %s",
+                                             A.host.size(), cudaGetErrorString(err));
+  }
   err = cudaMemcpy(dev, A.host.data(), A.host.size(), cudaMemcpyHostToDevice);
   if (err != cudaSuccess) {
     cudaFree(dev);
@@ -255,7 +295,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   g->is_star = d->is_star != 0;
   g->has_tab = has_tab;
   g->arena = dev;
-  g->arena_bytes = (int64_t)A.host.size();
+  g->arena_bytes = (int64_t)arena_bytes;
   auto fill_ref = [&](auto &R, size_t ol, size_t oc, size_t os, size_t ox, size_t om) {
     using T_ = std::remove_pointer_t<decltype(R.edge_len)>;
     R.n_edges = (int32_t)E;
@@ -293,7 +333,11 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
 int gsde_graph_destroy(gsde_graph *g) {
   if (!g) return GSDE_OK;
   DeviceGuard guard(g->device);
-  cudaError_t err = cudaFree(g->arena);
+  // like cudaFree, wait for queued kernels that may still read the arena
+  // (on any stream) before it can be recycled
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err == cudaSuccess && !arena_pool().give(g->device, g->arena, (size_t)g->arena_bytes))
+    err = cudaFree(g->arena);
   delete g;
   return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "graph_destroy");
 }
