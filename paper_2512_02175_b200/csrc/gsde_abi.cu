@@ -126,6 +126,8 @@ ArenaPool &arena_pool() {
   return *pool;
 }
 
+size_t g_is_general_size(int32_t is_star, int64_t S) { return is_star ? 0 : (size_t)S * 5; }
+
 struct Arena {
   std::vector<unsigned char> host;
   size_t add(const void *src, size_t bytes) {
@@ -258,6 +260,22 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     }
   }
 
+  // fat alias columns for general graphs (one L2 round trip per vertex event)
+  std::vector<int4> nfat(g_is_general_size(d->is_star, S));
+  if (!d->is_star) {
+    for (int64_t j = 0; j < S; ++j) {
+      const int4 c = ncol[j];
+      const int pe = c.y & 0x7fffffff, ae = c.z & 0x7fffffff;
+      int4 pe4, ae4;
+      memcpy(&pe4, &nedge[pe], sizeof(int4));
+      memcpy(&ae4, &nedge[ae], sizeof(int4));
+      nfat[5 * j + 0] = c;
+      nfat[5 * j + 1] = pe4;
+      nfat[5 * j + 2] = nedgev[pe];
+      nfat[5 * j + 3] = ae4;
+      nfat[5 * j + 4] = nedgev[ae];
+    }
+  }
   Arena A;
   const size_t o_len64 = A.add(len64.data(), E * 8), o_coef64 = A.add(coef64.data(), E * 8),
                o_sig64 = A.add(sig64.data(), E * 8), o_tabx64 = A.add(tabx64.data(), tabx64.size() * 8),
@@ -271,7 +289,8 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
                o_kind = A.add(kind.data(), E), o_taboff = A.add(taboff.data(), (E + 1) * 4),
                o_nedge = A.add(nedge.data(), E * sizeof(float4)),
                o_nedgev = A.add(nedgev.data(), E * sizeof(int4)),
-               o_ncol = A.add(ncol.data(), S * sizeof(int4));
+               o_ncol = A.add(ncol.data(), S * sizeof(int4)),
+               o_nfat = A.add(nfat.data(), nfat.size() * sizeof(int4));
   size_t arena_bytes = A.host.size();
   void *dev = arena_pool().take(device, A.host.size(), &arena_bytes);
   cudaError_t err = cudaSuccess;
@@ -320,6 +339,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   g->nat.edge = (const float4 *)P(o_nedge);
   g->nat.edgev = (const int4 *)P(o_nedgev);
   g->nat.col = (const int4 *)P(o_ncol);
+  g->nat.fat = d->is_star ? nullptr : (const int4 *)P(o_nfat);
   g->nat.tab_off = (const int32_t *)P(o_taboff);
   g->nat.tab_x = (const float *)P(o_tabx32);
   g->nat.tab_mu = (const float *)P(o_tabmu32);

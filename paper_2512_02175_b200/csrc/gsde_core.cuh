@@ -190,11 +190,15 @@ struct RefGraph {
 //   edgev: {init_off, init_deg, term_off, term_deg} of the endpoint vertices'
 //          alias columns (term_deg = 0 at the vertex at infinity).
 //   col:   alias column {thresh, prim, alias, 0}; prim/alias = edge | orient<<31.
+//   fat:   (general graphs read through L2) per alias column the column record
+//          followed by both candidates' {edge, edgev} records -- 5 x 16 B, so
+//          a vertex event is one dependent L2 round trip instead of two.
 struct NativeGraph {
   int32_t n_edges, n_slots;
   const float4 *edge;
   const int4 *edgev;
   const int4 *col;
+  const int4 *fat;  // [S][5]: {thresh, prim, alias, 0}, prim {edge, edgev}, alias {edge, edgev}
   const int32_t *tab_off;
   const float *tab_x, *tab_mu;
   int32_t has_tab;

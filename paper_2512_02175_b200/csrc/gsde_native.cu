@@ -129,6 +129,7 @@ struct Tables {
   const float4 *edge;
   const int4 *edgev;
   const int4 *col;
+  const int4 *fat;  // L2 path: fat alias columns
   __device__ __forceinline__ float4 E(int e) const { return SMEM ? edge[e] : __ldg(edge + e); }
   __device__ __forceinline__ int4 V(int e) const { return SMEM ? edgev[e] : __ldg(edgev + e); }
   __device__ __forceinline__ int4 C(int j) const { return SMEM ? col[j] : __ldg(col + j); }
@@ -202,6 +203,7 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, Share
   T.edge = G.edge;
   T.edgev = G.edgev;
   T.col = G.col;
+  T.fat = G.fat;
   if (SMEM) {
     float4 *se = reinterpret_cast<float4 *>(smem + off);
     off += (size_t)G.n_edges * sizeof(float4);
@@ -286,6 +288,23 @@ struct Lane {
       len = r.x;
       ev = T.V(e2);
     }
+    if (C::OCC) {
+      occ_off = (int)O.off[e2];
+      occ_top = (int)O.cnt[e2] - 1;
+      occ_inv = (float)(1.0 / O.dx[e2]);
+    }
+  }
+
+  // general graphs: install already-loaded records of edge e2
+  __device__ __forceinline__ void load_edge_rec(const Occ &O, int e2, float4 r, int4 v,
+                                                float sqdt) {
+    e = e2;
+    mu_a = r.y;
+    mu_b = r.z;
+    sig = r.w;
+    sig_sqdt = r.w * sqdt;
+    len = r.x;
+    ev = v;
     if (C::OCC) {
       occ_off = (int)O.off[e2];
       occ_top = (int)O.cnt[e2] - 1;
@@ -396,8 +415,23 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
     L.sq = fast_sqrt(L.dtr);
   }
   const bool at_init = !(L.x > 0.0f);
-  const int s = alias_pick(T, at_init ? L.ev.x : L.ev.z, at_init ? L.ev.y : L.ev.w, u);
-  L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
+  const int off = at_init ? L.ev.x : L.ev.z, deg = at_init ? L.ev.y : L.ev.w;
+  int s;
+  if constexpr (C::SMEM) {
+    s = alias_pick(T, off, deg, u);
+    L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
+  } else {  // one round trip: column + both candidates' records in flight together
+    uint32_t hi, lo;
+    mul_hilo(u, (uint32_t)deg, hi, lo);
+    const int4 *f = T.fat + 5 * (off + (int)hi);
+    const int4 c = __ldg(f), pe = __ldg(f + 1), pv = __ldg(f + 2), ae = __ldg(f + 3),
+               av = __ldg(f + 4);
+    const bool prim = lo < (uint32_t)c.x;
+    s = prim ? c.y : c.z;
+    const int4 er = prim ? pe : ae;
+    L.load_edge_rec(O, s & 0x7fffffff, *reinterpret_cast<const float4 *>(&er), prim ? pv : av,
+                    p.sqdt);
+  }
   L.x = s < 0 ? L.len : 0.0f;
   const float mu = L.drift(G, L.x);
   const float xn = fmaf(L.sig * L.sq, z, fmaf(mu, L.dtr, L.x));
