@@ -13,10 +13,15 @@
 //    per-edge constants and the accept test is 2-4 compares.  Everything else
 //    (vertex iterations, splits, reflections, statistics) is one divergent
 //    "rare" region per trip, followed by an explicit warp reconvergence;
-//  * RNG: one Philox4x32-10 block per TWO trips, counter (trip pair, domain,
-//    particle id) under the seed: words 0,1 -> Box-Muller -> the trips'
-//    Gaussians, words 2,3 -> the trips' 32-bit exit-slot uniforms.  Every
-//    trip consumes the same amount, so all lanes generate blocks in lockstep;
+//  * iterations of Q trips (Q = 10 by default); the first trip of each
+//    iteration is the vertex slot, the only trip that carries the divergent
+//    vertex region; lanes at a vertex wait for it, particles start on
+//    iteration boundaries, so the warp resolves its vertices together;
+//  * RNG: ceil((Q+1)/4) Philox4x32-10 blocks per iteration, counter
+//    (per-particle block index, domain, particle id) under the seed: word 0
+//    -> the vertex slot's 32-bit exit uniform, words 1..Q -> Box-Muller ->
+//    the Q trips' Gaussians.  Every iteration consumes the same amount, so
+//    all lanes generate blocks in lockstep;
 //  * exit slot: per-vertex alias table, one 16 B column record per pick;
 //  * star / small graphs: edge records and alias columns staged in shared
 //    memory; large networks read them through L2 (__ldg);
@@ -55,7 +60,7 @@ struct NatParams {
   double init_xmax;
   int32_t start_edge; // trials (general)
   float start_x;
-  int32_t rare_q;     // vertex trips only on trips t with t % rare_q == 0 (power of 2)
+  int32_t rare_q;     // ensemble: trips per iteration (vertex slot = first trip)
 };
 
 __device__ __forceinline__ float fast_sqrt(float v) {
@@ -364,12 +369,7 @@ struct Lane {
 template <class C>
 __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
                                           const Tables<C::SMEM> &T, const Occ &O,
-                                          const NatParams &p, float z, uint32_t u,
-                                          float xn_main) {
-  if (C::REFLECT && L.x > 0.0f) {  // free step beyond the mirror wall (kernels.py:185-188)
-    L.x = fmaxf(2.0f * p.reflect - xn_main, 0.0f);
-    return true;
-  }
+                                          const NatParams &p, float z, uint32_t u) {
   if (L.pend) {
     L.dtr = fmaxf(L.split_factor(G) * L.dtr, 0.0f);
     L.sq = fast_sqrt(L.dtr);
@@ -450,35 +450,36 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
 template <class C>
 __device__ __forceinline__ bool rare_trip(Lane<C> &L, const NativeGraph &G,
                                           const Tables<C::SMEM> &T, const Occ &O,
-                                          const NatParams &p, float z, uint32_t u,
-                                          float xn_main) {
+                                          const NatParams &p, float z, uint32_t u) {
   if constexpr (C::STAR)
-    return rare_star<C>(L, G, T, O, p, z, u, xn_main);
+    return rare_star<C>(L, G, T, O, p, z, u);
   else
     return rare_general<C>(L, G, T, O, p, z, u);
 }
 
-// One trip for every lane of the warp.  `live` lanes advance; returns true for
-// lanes whose macro step completed.
+// One trip for every lane of the warp: lanes with steps left advance; returns
+// true for lanes whose macro step completed.
 //
 // Common path: a lane strictly inside its edge always begins a fresh macro
-// step (dtr == dt), so the proposal uses cached constants.  Accepted: done.
-// Overshoot at an end: the hit is recorded with predicated moves (x = the
-// vertex, start point and Gaussian saved) and its split time is solved by
-// the lane's next vertex trip, so all vertex work is one divergent region.
-// Lanes at a vertex run that region only on vertex slots (trip index a
-// multiple of rare_q; a function of the particle's own trip counter).
-template <class C>
+// step (dtr == dt), so the proposal uses cached constants.  Accepted: done
+// (the star mirror wall reflects in place, kernels.py:185-188).  Overshoot
+// at an end: the hit is recorded with predicated moves (x = the vertex, start
+// point and Gaussian saved) and its split time is solved by the lane's next
+// vertex trip, so all vertex work is one divergent region.  That region is
+// compiled only into the vertex-slot trip (SLOT), the first trip of every
+// Q-trip iteration; lanes at a vertex wait for it, so the warp resolves its
+// vertices together.
+template <class C, bool SLOT>
 __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
                                      const Tables<C::SMEM> &T, const Shared &S, const Occ &O,
-                                     const NatParams &p, bool live, bool vertex_slot, float z,
-                                     uint32_t u) {
-  const float xn = fmaf(L.sig_sqdt, z, fmaf(L.drift(G, L.x), p.dt, L.x));
-  const bool check_hi = !C::STAR || C::REFLECT;
+                                     const NatParams &p, float z, uint32_t u) {
+  float xn = fmaf(L.sig_sqdt, z, fmaf(L.drift(G, L.x), p.dt, L.x));
+  const bool live = L.steps_left > 0;
   const bool run = live && (L.x > 0.0f) && (C::STAR || L.x < L.len);
   const bool lo_ok = xn > 0.0f;
-  const bool ok = run && lo_ok && (!check_hi || xn < L.len);
-  const bool hit = run && (C::STAR ? !lo_ok : !ok);
+  const bool ok = run && lo_ok && (C::STAR || xn < L.len);
+  const bool hit = run && !ok;
+  if (C::REFLECT && xn > L.len) xn = fmaxf(2.0f * L.len - xn, 0.0f);
   if (hit) {
     if (!C::STAR) L.M += 1;  // general counts hits; star counts vertex iterations
     L.pend = true;
@@ -488,11 +489,12 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
   }
   if (ok) L.x = xn;
   bool done = ok;
-  if (live && !ok && !hit && (vertex_slot || (C::REFLECT && L.x > 0.0f))) {
-    done = rare_trip<C>(L, G, T, O, p, z, u, xn);
+  if (SLOT && live && !run) {
+    done = rare_trip<C>(L, G, T, O, p, z, u);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
   if (C::OCC && done) L.occ_tick(O);
+  L.steps_left -= done ? 1 : 0;
   return done;
 }
 
@@ -526,9 +528,20 @@ __device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
   L.occ_left = O.start + O.every;
 }
 
-template <class C>
+// Random words of one Q-trip iteration: word 0 = the vertex-slot trip's exit
+// uniform, words 1..Q = Box-Muller inputs of the Q Gaussians; Philox blocks
+// (counter: per-particle block index, domain, particle id) are generated as
+// the trips need them.
+template <int Q>
+struct IterWords {
+  static constexpr int NB = (Q + 4) / 4;  // blocks per iteration
+  static_assert(Q % 2 == 0, "Gaussians come in Box-Muller pairs");
+};
+
+template <class C, int Q>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells) {
+  constexpr int NB = IterWords<Q>::NB;
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
@@ -544,17 +557,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
   L.pend = false;
   L.M = 0;
-  L.steps_left = 1;
+  L.steps_left = 0;  // no particle in flight: every trip is a no-op
   L.occ_left = 1 << 30;
-  uint32_t pair = 0;
+  uint32_t blk = 0;
   uint64_t id = 0;
   int64_t t_cross = 0, t_events = 0, t_truncs = 0;
-  // particles start only on warp iterations that are multiples of the
-  // vertex-slot period, so the lanes of a warp share their slot phase
-  const uint32_t q = (uint32_t)p.rare_q;
-  const uint32_t period = q > 2 ? q / 2 : 1;  // in trip pairs
-  bool waiting = i < p.n;                     // next particle not started yet
-  bool active = false;                        // a particle is in flight
+  bool waiting = i < p.n;  // next particle not started yet
+  bool active = false;     // a particle is in flight
 
   auto finish = [&]() {
     t_cross += L.cross;
@@ -571,26 +580,41 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       place_native(L, G, T, O, p, id, star_len);
       finish();
     }
+    L.steps_left = 0;
   }
 
-  for (uint32_t it = 0; __any_sync(0xffffffffu, active || waiting); ++it) {
-    if (waiting && (it & (period - 1)) == 0) {
+  // particles start on iteration boundaries, so the lanes of a warp share
+  // their vertex slot
+  while (__any_sync(0xffffffffu, active || waiting)) {
+    if (waiting) {
       id = (uint64_t)(p.id_offset + i);
       place_native(L, G, T, O, p, id, star_len);
-      pair = 0;
+      blk = 0;
       waiting = false;
       active = true;
     }
-    const uint32_t t0 = 2 * pair;
-    const Block r = native_block(p, pair++, kDomainEnsemble, id);
-    float z0, z1;
-    box_muller(r.x, r.y, z0, z1);
-    L.steps_left -= trip<C>(L, G, T, S, O, p, active, (t0 & (q - 1)) == 0, z0, r.z);
-    bool fin = active && L.steps_left == 0;
-    L.steps_left -= trip<C>(L, G, T, S, O, p, active && !fin, ((t0 + 1) & (q - 1)) == 0, z1,
-                            r.w);
-    fin = active && L.steps_left == 0;
-    if (fin) finish();
+    uint32_t W[4 * NB];
+    auto fill = [&](int kb) {
+      const Block r = native_block(p, blk + (uint32_t)kb, kDomainEnsemble, id);
+      W[4 * kb] = r.x;
+      W[4 * kb + 1] = r.y;
+      W[4 * kb + 2] = r.z;
+      W[4 * kb + 3] = r.w;
+    };
+    fill(0);
+#pragma unroll
+    for (int j = 0; j < Q; j += 2) {
+      if ((2 + j) / 4 != j / 4) fill((2 + j) / 4);
+      float z0, z1;
+      box_muller(W[1 + j], W[2 + j], z0, z1);
+      if (j == 0)
+        trip<C, true>(L, G, T, S, O, p, z0, W[0]);
+      else
+        trip<C, false>(L, G, T, S, O, p, z0, 0u);
+      trip<C, false>(L, G, T, S, O, p, z1, 0u);
+    }
+    blk += NB;
+    if (active && L.steps_left == 0) finish();
   }
   if (o.totals) {
     warp_add_i64(&o.totals[0], t_cross);
@@ -657,8 +681,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
     bool fin = false;
-    if (active) fin = rare_trip<C>(L, G, T, O, p, z0, r.z, 0.0f);
-    if (active && !fin) fin = rare_trip<C>(L, G, T, O, p, z1, r.w, 0.0f);
+    if (active) fin = rare_trip<C>(L, G, T, O, p, z0, r.z);
+    if (active && !fin) fin = rare_trip<C>(L, G, T, O, p, z1, r.w);
     if (fin) finish();
   }
   if (o.totals) {
@@ -725,16 +749,15 @@ int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items) {
   return (int)(need < full ? (need < 1 ? 1 : need) : full);
 }
 
-// Vertex-slot period of the ensemble kernel (power of two; GSDE_RARE_Q overrides).
+// Trips per iteration of the ensemble kernel (the vertex-slot period):
+// GSDE_RARE_Q=6|14 overrides the default 10.
 int32_t rare_period() {
-  static int32_t q = [] {
+  static const int32_t env = [] {
     const char *e = getenv("GSDE_RARE_Q");
-    int v = e ? atoi(e) : 4;
-    int r = 1;
-    while (r < v && r < 64) r <<= 1;
-    return r;
+    return e ? atoi(e) : 0;
   }();
-  return q;
+  if (env == 6 || env == 14) return env;
+  return 10;  // 11 of 12 words used; best or within 1% on star3 / hub64 / vascular
 }
 
 NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
@@ -774,8 +797,9 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool reflect, F &&f) {
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
     constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
-    if (ST && reflect)
-      return tab ? f(Cfg<ST, SM, true, true, OCC>{}) : f(Cfg<ST, SM, false, true, OCC>{});
+    if constexpr (ST)
+      if (reflect)
+        return tab ? f(Cfg<ST, SM, true, true, OCC>{}) : f(Cfg<ST, SM, false, true, OCC>{});
     return tab ? f(Cfg<ST, SM, true, false, OCC>{}) : f(Cfg<ST, SM, false, false, OCC>{});
   };
   if (star) return smem ? with(T{}, T{}) : with(T{}, N{});
@@ -800,7 +824,9 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   const int64_t n = a.n_particles;
   auto run = [&](auto cfg) -> cudaError_t {
     using C = decltype(cfg);
-    auto k = native_ensemble_kernel<C>;
+    auto k = p.rare_q == 6    ? native_ensemble_kernel<C, 6>
+             : p.rare_q == 14 ? native_ensemble_kernel<C, 14>
+                              : native_ensemble_kernel<C, 10>;
     // occupation counters in shared memory when the grid is small and no
     // per-block count can overflow 32 bits
     int occ_cells = 0;
