@@ -2,8 +2,8 @@
 //
 // Design:
 //  * one particle per lane, persistent grid (SMs x resident CTAs), particles
-//    assigned by grid stride; all per-particle state lives in registers for
-//    the whole run;
+//    handed out dynamically (warp-aggregated atomic on a grid-wide counter);
+//    all per-particle state lives in registers for the whole run;
 //  * flattened state machine: every loop trip performs exactly one proposal
 //    per lane -- a free Euler-Maruyama step or one vertex iteration -- so the
 //    split / excursion loops of kernels.py:198-220 and :257-288 become extra
@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMinBlocks = 4;  // caps registers at 64 -> 32 warps / SM
+constexpr int kMinBlocksTrials = 5;  // trials carry less state: <= 51 registers -> 40 warps / SM
 constexpr int kPriv = 8;       // lane-private M-histogram bins
 constexpr uint32_t kDomainEnsemble = 0u;
 constexpr uint32_t kDomainTrials = 1u;
@@ -540,7 +541,8 @@ struct IterWords {
 
 template <class C, int Q>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
-    native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells) {
+    native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
+                           unsigned long long *work) {
   constexpr int NB = IterWords<Q>::NB;
   const int nb = p.cap + 1;
   Shared S;
@@ -564,28 +566,49 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   int64_t t_cross = 0, t_events = 0, t_truncs = 0;
   bool waiting = i < p.n;  // next particle not started yet
   bool active = false;     // a particle is in flight
+  bool need = false;       // finished: fetch the next particle id
 
   auto finish = [&]() {
     t_cross += L.cross;
     t_events += L.events;
     t_truncs += L.truncs;
     ensemble_epilogue(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
-    i += stride;
     active = false;
-    waiting = i < p.n;
+    need = true;
   };
   if (p.n_steps == 0) {  // placement only (engine.py:329-336)
     while (waiting) {
       id = (uint64_t)(p.id_offset + i);
       place_native(L, G, T, O, p, id, star_len);
       finish();
+      i += stride;
+      waiting = i < p.n;
     }
+    need = false;
     L.steps_left = 0;
   }
 
-  // particles start on iteration boundaries, so the lanes of a warp share
-  // their vertex slot
-  while (__any_sync(0xffffffffu, active || waiting)) {
+  // First particle: the thread index; then dynamic, from a grid-wide counter
+  // with one warp-aggregated atomic per batch of finishing lanes, so warps
+  // the schedulers favour take more particles and the SMs stay full until the
+  // end (results are per particle id and integer sums: assignment-invariant).
+  // Particles start on iteration boundaries, so the lanes of a warp share
+  // their vertex slot.
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    if (nm) {
+      const int leader = __ffs(nm) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(work, (unsigned long long)__popc(nm));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        i = stride + (int64_t)base + __popc(nm & ((1u << lane) - 1u));
+        waiting = i < p.n;
+        need = false;
+      }
+    }
+    if (!__any_sync(0xffffffffu, active || waiting)) break;
     if (waiting) {
       id = (uint64_t)(p.id_offset + i);
       place_native(L, G, T, O, p, id, star_len);
@@ -627,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
 // fused exit counts per edge and M histogram including M = 0.
 template <class C>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+__global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv) {
   const int nb = p.cap + 1;
   Shared S;
@@ -841,7 +864,14 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
       if (per_block >= 4.0e9) occ_cells = 0;
     }
     smem = smem_bytes(g, a.cap + 1, stage, false, occ_cells);
-    return launch(k, smem, grid, s, g->nat, p, o, occ_cells);
+    // grid-wide particle counter (stream-ordered scratch: calls stay re-entrant)
+    unsigned long long *work = nullptr;
+    err = cudaMallocAsync(reinterpret_cast<void **>(&work), sizeof(*work), s);
+    if (err != cudaSuccess) return err;
+    err = cudaMemsetAsync(work, 0, sizeof(*work), s);
+    if (err == cudaSuccess) err = launch(k, smem, grid, s, g->nat, p, o, occ_cells, work);
+    const cudaError_t ferr = cudaFreeAsync(work, s);
+    return err != cudaSuccess ? err : ferr;
   };
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run)
              : dispatch<false>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run);
