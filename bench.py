@@ -199,7 +199,8 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML in-process,
+    every 50 ms; nvidia-smi subprocesses only if NVML is unavailable)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -211,18 +212,41 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            bits = (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+            def sample():
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                return [str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), str(mx)] + [
+                    "Active" if r & b else "Not Active" for b in bits]
+            sample()
+            return sample
+        except Exception:
+            return None
+
+    def _smi(self):
+        out = subprocess.run(
+            ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        return [p.strip() for p in out.stdout.strip().split(",")]
+
     def _run(self):
+        sample = self._nvml() or self._smi
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                parts = sample()
                 if len(parts) == 6:
                     self.samples.append(parts)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -345,6 +369,9 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+STEP_MS = []  # per-step device times of the last time_workload call
+
+
 def time_workload(wl, steps, warmup, dist, torch, dev, flush_buf, clocks_index=None):
     """Returns (elapsed_s max over ranks, kernel_s, res, launches)."""
     from paper_2512_02175_b200 import _native
@@ -359,12 +386,17 @@ def time_workload(wl, steps, warmup, dist, torch, dev, flush_buf, clocks_index=N
         dist.barrier()
     torch.cuda.synchronize(dev)
     l0 = _native.launch_count()
+    STEP_MS.clear()
     total = 0.0
     kern = 0.0
     sampler = ClockSampler(clocks_index) if clocks_index is not None else None
     if sampler:
         sampler.__enter__()
     try:
+        # steps are enqueued back to back (no host sync inside the loop), so the
+        # host-side launch work overlaps the previous step and never sits
+        # between a start event and its kernel
+        ev = []
         for _ in range(steps):
             flush_l2(flush_buf)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -376,9 +408,12 @@ def time_workload(wl, steps, warmup, dist, torch, dev, flush_buf, clocks_index=N
             if dist is not None:
                 dist.all_reduce(wl.reduce_tensor(res))
             e2.record(stream)
+            ev.append((e0, e1, e2, res))
+        for e0, e1, e2, _ in ev:
             e2.synchronize()
             total += e0.elapsed_time(e2) / 1e3
             kern += e0.elapsed_time(e1) / 1e3
+            STEP_MS.append(round(e0.elapsed_time(e2), 3))
     finally:
         if sampler:
             sampler.__exit__()
@@ -469,6 +504,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+            "step_ms": list(STEP_MS),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded graph generators, random streams; no external data)",
             "config": dict(wl.config(), parallelism=f"particle-sharded x{world}",

@@ -16,7 +16,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsde.so")
+# GSDE_LIB_PATH: an alternative build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("GSDE_LIB_PATH") or os.path.join(_HERE, "libgsde.so")
 
 GSDE_STREAM_NATIVE = 0
 GSDE_STREAM_REFERENCE = 1

@@ -291,6 +291,8 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
                o_nedgev = A.add(nedgev.data(), E * sizeof(int4)),
                o_ncol = A.add(ncol.data(), S * sizeof(int4)),
                o_nfat = A.add(nfat.data(), nfat.size() * sizeof(int4));
+  const std::vector<unsigned long long> work(gsde_graph::kWorkSlots, 0ull);
+  const size_t o_work = A.add(work.data(), work.size() * sizeof(unsigned long long));
   size_t arena_bytes = A.host.size();
   void *dev = arena_pool().take(device, A.host.size(), &arena_bytes);
   cudaError_t err = cudaSuccess;
@@ -315,6 +317,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   g->has_tab = has_tab;
   g->arena = dev;
   g->arena_bytes = (int64_t)arena_bytes;
+  g->work = (unsigned long long *)P(o_work);
   auto fill_ref = [&](auto &R, size_t ol, size_t oc, size_t os, size_t ox, size_t om) {
     using T_ = std::remove_pointer_t<decltype(R.edge_len)>;
     R.n_edges = (int32_t)E;

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/gsde.h"
 #include "gsde_core.cuh"
 
@@ -18,6 +20,13 @@ struct gsde_graph_s {
   gsde::NativeGraph nat{};
   // native smem staging size for the whole graph (0 = too large, read via L2)
   int64_t nat_graph_smem = 0;
+  // work-distribution counters of the native kernels: a ring of slots in the
+  // arena, one per call (zeroed stream-ordered before the launch), so up to
+  // kWorkSlots calls on one handle may be in flight on different streams
+  static constexpr int kWorkSlots = 64;
+  unsigned long long *work = nullptr;
+  std::atomic<uint32_t> work_ticket{0};
+  unsigned long long *next_work_slot() { return work + (work_ticket++ % kWorkSlots); }
 };
 
 namespace gsde {

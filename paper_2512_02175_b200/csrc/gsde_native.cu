@@ -39,7 +39,10 @@ namespace gsde {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMinBlocks = 4;  // caps registers at 64 -> 32 warps / SM
+#ifndef GSDE_MIN_BLOCKS
+#define GSDE_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocks = GSDE_MIN_BLOCKS;  // 4: caps registers at 64 -> 32 warps / SM
 constexpr int kMinBlocksTrials = 5;  // trials carry less state: <= 51 registers -> 40 warps / SM
 constexpr int kPriv = 8;       // lane-private M-histogram bins
 constexpr uint32_t kDomainEnsemble = 0u;
@@ -94,22 +97,23 @@ __device__ __forceinline__ float fast_rcp(float v) {
   return r;
 }
 
-// kernels.py:88-131 in FP32, branch-free: first s >= 0 with a s^2 + b s + c = 0,
-// clamped to 1; -1 if none.  c < 0 -> 0; c == 0 -> 0 if b <= 0, else the
-// nonzero root -b/a when a < 0, else -1; otherwise the smallest nonnegative
-// of the stable pair q/a, c/q with q = -(b + sign(b) sqrt(disc)) / 2 (a = 0
-// falls out as q/a = +-inf, c/q = -c/b).
-__device__ __forceinline__ float solve_bf(float a, float b, float c) {
-  const float inf = __int_as_float(0x7f800000);
-  const float sq = fast_sqrt(fmaxf(b * b - 4.0f * a * c, 0.0f));
-  const float q = -0.5f * (b + copysignf(sq, b));
-  const float ra = fast_rcp(a);
-  const float r1 = q * ra;
-  const float r2 = c * fast_rcp(q);
-  float s = fminf(r1 >= 0.0f ? r1 : inf, (q != 0.0f && r2 >= 0.0f) ? r2 : inf);
-  s = s == inf ? -1.0f : fminf(s, 1.0f);
-  const float s0 = b <= 0.0f ? 0.0f : (a >= 0.0f ? -1.0f : fminf(-b * ra, 1.0f));
-  return c < 0.0f ? 0.0f : (c == 0.0f ? s0 : s);
+// Split time of an overshooting proposal, FP32, branch-free.  Callers ask
+// only when the proposal x' = c + a + b reached the vertex at distance c >= 0
+// (a + b + c <= 0).  For c > 0, a s^2 + b s + c then has exactly one root in
+// (0, 1] and it is the reference's answer -- the smallest non-negative root
+// clamped to 1, -1 (-> 1) if none (kernels.py:88-131, :191-192).  Both cases
+// of that root without cancellation, D = b^2 - 4ac:
+//   b <  0:  s = 2c / (|b| + sqrt(D))
+//   b >= 0:  s = (|b| + sqrt(D)) / (-2a)      (overshoot forces a < 0)
+// c = 0 (a zero-time re-hit from the vertex): b <= 0 -> 0 (kernels.py:99-107);
+// b > 0 falls out of the second form as -b/a.  Rounding that leaves [0, 1]
+// (or NaN) falls back to 1.
+__device__ __forceinline__ float split_root(float a, float b, float c) {
+  const float t = fabsf(b) + fast_sqrt(fmaxf(fmaf(b, b, -4.0f * a * c), 0.0f));
+  const bool neg = b < 0.0f;
+  const float s = (neg ? 2.0f * c : t) * fast_rcp(neg ? t : -2.0f * a);
+  if (c == 0.0f && b <= 0.0f) return 0.0f;
+  return (s >= 0.0f && s <= 1.0f) ? s : 1.0f;
 }
 
 // Philox4x32-10 with the key schedule precomputed in the kernel parameters:
@@ -330,8 +334,7 @@ struct Lane {
     const float a = drift(G, px) * dtr;
     const float b = (sig * sq) * pz;
     const bool lo = C::STAR || !(x > 0.0f);
-    float s = lo ? solve_bf(a, b, px) : solve_bf(-a, -b, len - px);
-    s = s < 0.0f ? 1.0f : s;
+    const float s = lo ? split_root(a, b, px) : split_root(-a, -b, len - px);
     return 1.0f - s * s;
   }
 
@@ -864,14 +867,13 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
       if (per_block >= 4.0e9) occ_cells = 0;
     }
     smem = smem_bytes(g, a.cap + 1, stage, false, occ_cells);
-    // grid-wide particle counter (stream-ordered scratch: calls stay re-entrant)
-    unsigned long long *work = nullptr;
-    err = cudaMallocAsync(reinterpret_cast<void **>(&work), sizeof(*work), s);
-    if (err != cudaSuccess) return err;
+    // grid-wide particle counter: this call's slot of the handle's ring
+    // (a per-call cudaMallocAsync here stalled running kernels for up to
+    // hundreds of ms when the pool remapped memory)
+    unsigned long long *work = const_cast<gsde_graph *>(g)->next_work_slot();
     err = cudaMemsetAsync(work, 0, sizeof(*work), s);
-    if (err == cudaSuccess) err = launch(k, smem, grid, s, g->nat, p, o, occ_cells, work);
-    const cudaError_t ferr = cudaFreeAsync(work, s);
-    return err != cudaSuccess ? err : ferr;
+    if (err != cudaSuccess) return err;
+    return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work);
   };
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run)
              : dispatch<false>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run);

@@ -241,9 +241,7 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
         raise ConfigInvalid("the occupation histogram needs a grid")
     if grid is not None:
         res["hist"] = torch.zeros(grid.n_cells, dtype=torch.int64, **kw)
-        g_off = torch.tensor(grid.offsets, **kw)
-        g_cnt = torch.tensor(grid.counts, **kw)
-        g_dx = torch.tensor(grid.dx, **kw)
+        g_off, g_cnt, g_dx = grid.device_arrays(torch, dev)
         res["_grid"] = (g_off, g_cnt, g_dx)
         o.hist, o.hist_offsets, o.hist_counts, o.hist_dx = (
             res["hist"].data_ptr(), g_off.data_ptr(), g_cnt.data_ptr(), g_dx.data_ptr())
