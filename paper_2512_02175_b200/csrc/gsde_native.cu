@@ -13,15 +13,14 @@
 //    per-edge constants and the accept test is 2-4 compares.  Everything else
 //    (vertex iterations, splits, reflections, statistics) is one divergent
 //    "rare" region per trip, followed by an explicit warp reconvergence;
-//  * iterations of Q trips (Q = 10 by default); the first trip of each
-//    iteration is the vertex slot, the only trip that carries the divergent
-//    vertex region; lanes at a vertex wait for it, particles start on
-//    iteration boundaries, so the warp resolves its vertices together;
-//  * RNG: ceil((Q+1)/4) Philox4x32-10 blocks per iteration, counter
-//    (per-particle block index, domain, particle id) under the seed: word 0
-//    -> the vertex slot's 32-bit exit uniform, words 1..Q -> Box-Muller ->
-//    the Q trips' Gaussians.  Every iteration consumes the same amount, so
-//    all lanes generate blocks in lockstep;
+//  * iterations of Q = 14 trips; the vertex slots (trip 0, and trip 7 on
+//    general graphs) are the only trips that carry the divergent vertex
+//    region; lanes at a vertex wait for a slot, particles start on iteration
+//    boundaries, so the warp resolves its vertices together;
+//  * RNG: 4 Philox4x32-10 blocks per iteration, counter (per-particle block
+//    index, domain, particle id) under the seed: 14 words -> Box-Muller ->
+//    the trips' Gaussians, one 32-bit exit uniform per slot.  Every iteration
+//    consumes the same amount, so all lanes generate blocks in lockstep;
 //  * exit slot: per-vertex alias table, one 16 B column record per pick;
 //  * star / small graphs: edge records and alias columns staged in shared
 //    memory; large networks read them through L2 (__ldg);
@@ -45,6 +44,7 @@ constexpr int kThreads = 256;
 constexpr int kMinBlocks = GSDE_MIN_BLOCKS;  // 4: caps registers at 64 -> 32 warps / SM
 constexpr int kMinBlocksTrials = 5;  // trials carry less state: <= 51 registers -> 40 warps / SM
 constexpr int kPriv = 8;       // lane-private M-histogram bins
+constexpr int kTrips = 14;     // ensemble: trips per iteration
 constexpr uint32_t kDomainEnsemble = 0u;
 constexpr uint32_t kDomainTrials = 1u;
 constexpr uint32_t kDomainPlace = 0xFFFFFFFFu;
@@ -64,7 +64,6 @@ struct NatParams {
   double init_xmax;
   int32_t start_edge; // trials (general)
   float start_x;
-  int32_t rare_q;     // ensemble: trips per iteration (vertex slot = first trip)
 };
 
 __device__ __forceinline__ float fast_sqrt(float v) {
@@ -532,21 +531,39 @@ __device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
   L.occ_left = O.start + O.every;
 }
 
-// Random words of one Q-trip iteration: word 0 = the vertex-slot trip's exit
-// uniform, words 1..Q = Box-Muller inputs of the Q Gaussians; Philox blocks
-// (counter: per-particle block index, domain, particle id) are generated as
-// the trips need them.
-template <int Q>
+// Random words of one Q-trip iteration with SLOTS vertex slots (trips
+// k Q / SLOTS): word 0 = slot 0's exit uniform, words 1..Q = Box-Muller
+// inputs of the Q Gaussians, word 4 NB - k = slot k's uniform (k >= 1).
+// Philox blocks (counter: per-particle block index, domain, particle id) are
+// generated as the trips need them; every helper below folds to a constant
+// once the trip loop is unrolled.
+template <int Q, int SLOTS>
 struct IterWords {
-  static constexpr int NB = (Q + 4) / 4;  // blocks per iteration
+  static constexpr int NB = (Q + SLOTS + 3) / 4;  // blocks per iteration
   static_assert(Q % 2 == 0, "Gaussians come in Box-Muller pairs");
+  static_assert(SLOTS >= 1 && SLOTS <= 4 && Q % SLOTS == 0, "slots split the iteration evenly");
+  __host__ __device__ static constexpr bool is_slot(int t) { return t % (Q / SLOTS) == 0; }
+  __host__ __device__ static constexpr int uword(int t) {  // uniform word of slot trip t
+    return t == 0 ? 0 : 4 * NB - t / (Q / SLOTS);
+  }
+  // bit b set: block b is read by some trip of the pairs 0..j
+  __host__ __device__ static constexpr unsigned need(int j) {
+    unsigned m = 0;
+    for (int jj = 0; jj <= j; jj += 2) {
+      m |= (1u << ((1 + jj) / 4)) | (1u << ((2 + jj) / 4));
+      if (is_slot(jj)) m |= 1u << (uword(jj) / 4);
+      if (is_slot(jj + 1)) m |= 1u << (uword(jj + 1) / 4);
+    }
+    return m;
+  }
 };
 
-template <class C, int Q>
+template <class C, int Q, int SLOTS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
                            unsigned long long *work) {
-  constexpr int NB = IterWords<Q>::NB;
+  using IW = IterWords<Q, SLOTS>;
+  constexpr int NB = IW::NB;
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
@@ -627,17 +644,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       W[4 * kb + 2] = r.z;
       W[4 * kb + 3] = r.w;
     };
-    fill(0);
 #pragma unroll
     for (int j = 0; j < Q; j += 2) {
-      if ((2 + j) / 4 != j / 4) fill((2 + j) / 4);
+      const unsigned fresh = IW::need(j) & ~(j ? IW::need(j - 2) : 0u);
+#pragma unroll
+      for (int kb = 0; kb < NB; ++kb)
+        if (fresh & (1u << kb)) fill(kb);
       float z0, z1;
       box_muller(W[1 + j], W[2 + j], z0, z1);
-      if (j == 0)
-        trip<C, true>(L, G, T, S, O, p, z0, W[0]);
+      if (IW::is_slot(j))
+        trip<C, true>(L, G, T, S, O, p, z0, W[IW::uword(j)]);
       else
         trip<C, false>(L, G, T, S, O, p, z0, 0u);
-      trip<C, false>(L, G, T, S, O, p, z1, 0u);
+      if (IW::is_slot(j + 1))
+        trip<C, true>(L, G, T, S, O, p, z1, W[IW::uword(j + 1)]);
+      else
+        trip<C, false>(L, G, T, S, O, p, z1, 0u);
     }
     blk += NB;
     if (active && L.steps_left == 0) finish();
@@ -775,21 +797,9 @@ int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items) {
   return (int)(need < full ? (need < 1 ? 1 : need) : full);
 }
 
-// Trips per iteration of the ensemble kernel (the vertex-slot period):
-// GSDE_RARE_Q=6|14 overrides the default 10.
-int32_t rare_period() {
-  static const int32_t env = [] {
-    const char *e = getenv("GSDE_RARE_Q");
-    return e ? atoi(e) : 0;
-  }();
-  if (env == 6 || env == 14) return env;
-  return 10;  // 11 of 12 words used; best or within 1% on star3 / hub64 / vascular
-}
-
 NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
   NatParams p{};
   p.seed = seed;
-  p.rare_q = 1;
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   for (int r = 0; r < 10; ++r, k0 += kPhiloxW0, k1 += kPhiloxW1) {
     p.rk[2 * r] = k0;
@@ -843,16 +853,19 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   p.init_edge = (int32_t)a.init_edge;
   p.init_x = (float)a.init_x;
   p.init_xmax = a.init_xmax;
-  p.rare_q = rare_period();
   const bool stage = g->nat_graph_smem > 0;
   const bool occ = o.occ != nullptr;
   const int d = g->device;
   const int64_t n = a.n_particles;
   auto run = [&](auto cfg) -> cudaError_t {
     using C = decltype(cfg);
-    auto k = p.rare_q == 6    ? native_ensemble_kernel<C, 6>
-             : p.rare_q == 14 ? native_ensemble_kernel<C, 14>
-                              : native_ensemble_kernel<C, 10>;
+    // 14-trip iterations; one vertex slot on star graphs (rare, short vertex
+    // visits), two on general graphs (a zero-time re-hit makes a lane wait for
+    // the next slot).  Measured: (10,1) / (14,1) / (18,1) /
+    // (22,1) on star3, (10,2) / (14,2) / (22,2) / (12,3) / (18,3) / (16,4)
+    // on hub64 and vascular.
+    constexpr int kSlots = C::STAR ? 1 : 2;
+    auto k = native_ensemble_kernel<C, kTrips, kSlots>;
     // occupation counters in shared memory when the grid is small and no
     // per-block count can overflow 32 bits
     int occ_cells = 0;
