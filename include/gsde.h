@@ -38,9 +38,10 @@ enum {
  *  INJECT:    draws supplied by the caller per (particle, draw index) --
  *             raw 64-bit words for uniforms, reference normals for Gaussians
  *             -- arithmetic in FP32 or FP64 (`precision`).
- *  NATIVE:    the B200 production stream -- FP32, one Philox4x32-10 block per
- *             two proposals (Box-Muller Gaussian + 32-bit uniform each), alias
- *             tables for exit slots, flattened per-lane state machine.
+ *  NATIVE:    the B200 production stream -- FP32, Philox4x32-10 feeding
+ *             Box-Muller Gaussians per proposal and 32-bit uniforms per vertex
+ *             slot, alias tables for exit slots, flattened per-lane state
+ *             machine in 14-proposal iterations.
  *             Statistically equivalent, not bit-identical, to REFERENCE. */
 enum { GSDE_STREAM_NATIVE = 0, GSDE_STREAM_REFERENCE = 1, GSDE_STREAM_INJECT = 2 };
 enum { GSDE_PREC_F32 = 0, GSDE_PREC_F64 = 1 };
@@ -187,6 +188,42 @@ int gsde_step_batch(const gsde_graph *g, const gsde_step_args *a, int64_t *edge,
 int gsde_histogram(int64_t n, const int64_t *edge, const double *x, const int64_t *offsets,
                    const int64_t *counts, const double *dx, int64_t n_cells, int64_t *hist,
                    void *stream);
+
+/* Finite-volume Fokker-Planck baseline (fvm.py): the packed static arrays of
+ * fvm._pack_static (fvm.py:343-382) plus an ownership split of the vertex
+ * exchange, all DEVICE pointers.  Vertex v's slots are v_off[v]..v_off[v+1];
+ * owned[c] = 1 when cell c is the vertex-adjacent cell of a vertex of degree
+ * >= 2 (its update is done by that vertex's thread); vpar lists the vertices
+ * whose cells no other vertex touches, vser (ascending) the rest (cells shared
+ * through single-cell edges), which one thread processes in vertex order. */
+typedef struct {
+  int64_t n_edges, n_cells, n_vertices, n_vpar, n_vser;
+  const int64_t *offs;       /* [E+1] grid offsets */
+  const double *dx_edge;     /* [E] cell width */
+  const double *D_edge;      /* [E] sigma^2 / 2 */
+  const double *face_mu;     /* [F] drift on interior faces, edge-major */
+  const int64_t *face_off;   /* [E+1] */
+  const int64_t *v_off;      /* [V+1] */
+  const int64_t *v_cells;    /* [S] vertex-adjacent cell per slot */
+  const double *v_b;         /* [S] jump weight */
+  const double *v_dx;        /* [S] */
+  const double *v_speed_in;  /* [S] inward drift speed (>= 0) */
+  const double *v_D;         /* [S] */
+  const int64_t *cell_edge;  /* [C] edge of each cell */
+  const uint8_t *owned;      /* [C] */
+  const int64_t *vpar;       /* [n_vpar] */
+  const int64_t *vser;       /* [n_vser] ascending */
+} gsde_fvm_desc;
+
+/* fvm_run's stepper (_fvm_step_loop, fvm.py:254-340): n_steps explicit Euler
+ * steps of rho (device [n_cells], updated in place; scratch: device
+ * [n_cells]) in the reference's floating-point operation order (bit-identical
+ * FP64).  After each step the run stops if min(0, min rho) <
+ * neg_floor * max(1, max |rho|); *neg_step (device int64) receives the
+ * 1-based step index, 0 if none.  red: caller-owned device scratch of 8
+ * uint64.  One persistent cooperative kernel, one grid barrier per step. */
+int gsde_fvm_run(const gsde_fvm_desc *d, double *rho, double *scratch, int64_t n_steps,
+                 double dt, double neg_floor, int64_t *neg_step, uint64_t *red, void *stream);
 
 /* Native reader for the "metric-graph v1" text format (graphfile.py:69-186),
  * happy path only: returns GSDE_OK and an opaque result, or a nonzero code for

@@ -554,3 +554,79 @@ void orc_fill_draws_rows(const uint64_t *seed, const uint64_t *pid, const uint64
       nrm[i * K + j] = orc_u64_to_normal(r);
     }
 }
+
+/* Finite-volume Fokker-Planck stepper: restatement of _fvm_step_loop
+ * (fvm.py:254-340) over the packed arrays of _pack_static (fvm.py:343-382).
+ * Explicit Euler, upwind drift + central diffusion on interior faces, then
+ * the pairwise vertex exchange; rho updated in place.  Returns the 1-based
+ * step at which min(0, min rho) < neg_floor * max(1, max |rho|), 0 if none
+ * (the state is left at that step, like the reference). */
+int64_t orc_fvm_steps(double *rho, int64_t n_cells, int64_t n_steps, double dt,
+                      const int64_t *offs, int64_t n_edges, const double *dx_edge,
+                      const double *D_edge, const double *face_mu, const int64_t *face_off,
+                      const int64_t *v_off, int64_t n_vertices, const int64_t *v_cells,
+                      const double *v_b, const double *v_dx, const double *v_speed_in,
+                      const double *v_D, double neg_floor) {
+  double *nw = (double *)malloc((size_t)(n_cells > 0 ? n_cells : 1) * sizeof(double));
+  int64_t result = 0;
+  for (int64_t step = 0; step < n_steps && !result; ++step) {
+    for (int64_t i = 0; i < n_cells; ++i) nw[i] = rho[i];
+    for (int64_t e = 0; e < n_edges; ++e) { /* interior faces, fvm.py:282-295 */
+      const int64_t lo = offs[e], hi = offs[e + 1];
+      const double dx = dx_edge[e], D = D_edge[e], scale = dt / dx;
+      for (int64_t j = lo + 1; j < hi; ++j) {
+        const double mu = face_mu[face_off[e] + (j - lo - 1)];
+        double F = mu > 0.0 ? mu * rho[j - 1] : mu * rho[j];
+        F -= D * (rho[j] - rho[j - 1]) / dx;
+        nw[j] += scale * F;
+        nw[j - 1] -= scale * F;
+      }
+    }
+    for (int64_t v = 0; v < n_vertices; ++v) { /* vertex exchange, fvm.py:296-328 */
+      const int64_t lo = v_off[v], hi = v_off[v + 1];
+      if (hi - lo < 2) continue;
+      for (int64_t i = lo; i < hi; ++i) {
+        const int64_t ci = v_cells[i];
+        const double bi = v_b[i], rho_i = rho[ci];
+        if (v_speed_in[i] > 0.0) {
+          const double others = 1.0 - bi;
+          if (others > 0.0) {
+            const double total = v_speed_in[i] * rho_i;
+            for (int64_t j = lo; j < hi; ++j) {
+              if (j == i) continue;
+              const double f = total * v_b[j] / others;
+              nw[v_cells[j]] += dt * f / v_dx[j];
+              nw[ci] -= dt * f / v_dx[i];
+            }
+          }
+        }
+        const double conc_i = rho_i / bi;
+        for (int64_t j = i + 1; j < hi; ++j) {
+          const int64_t cj = v_cells[j];
+          const double dpair = 0.5 * (v_D[i] + v_D[j]);
+          const double dxh = 2.0 * v_dx[i] * v_dx[j] / (v_dx[i] + v_dx[j]);
+          const double g = dpair * (conc_i - rho[cj] / v_b[j]) / dxh;
+          if (g >= 0.0) {
+            const double f = g * v_b[j];
+            nw[cj] += dt * f / v_dx[j];
+            nw[ci] -= dt * f / v_dx[i];
+          } else {
+            const double f = -g * v_b[i];
+            nw[ci] += dt * f / v_dx[i];
+            nw[cj] -= dt * f / v_dx[j];
+          }
+        }
+      }
+    }
+    double mx = 1.0, mn = 0.0; /* fvm.py:329-337 */
+    for (int64_t i = 0; i < n_cells; ++i) {
+      rho[i] = nw[i];
+      const double a = fabs(rho[i]);
+      if (a > mx) mx = a;
+      if (rho[i] < mn) mn = rho[i];
+    }
+    if (mn < neg_floor * mx) result = step + 1;
+  }
+  free(nw);
+  return result;
+}

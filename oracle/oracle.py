@@ -69,6 +69,9 @@ def lib():
                                               P, i32]
         L.orc_fill_draws.argtypes = [u64, u64, i64, u64, i64, P, P, i32]
         L.orc_fill_draws_rows.argtypes = [P, P, P, i64, i64, P, P]
+        L.orc_fvm_steps.restype = i64
+        L.orc_fvm_steps.argtypes = [P, i64, i64, f64, P, i64, P, P, P, P, P, i64, P, P, P, P, P,
+                                    f64]
         _lib = L
     return _lib
 
@@ -224,3 +227,20 @@ def ensemble_occupation(og: OracleGraph, seed, n, n_steps, dt, offsets, counts, 
                                   _ptr(offsets), _ptr(counts), _ptr(dx), every, start, _ptr(occ),
                                   threads)
     return occ
+
+
+def fvm_steps(rho, n_steps, dt, packed, neg_floor=-1e-10):
+    """_fvm_step_loop restated in C: advances ``rho`` (copied) over the
+    ``_pack_static`` tuple; returns (rho, 1-based negative step or 0)."""
+    i8, f8 = np.int64, np.float64
+    kinds = (i8, f8, f8, f8, i8, i8, i8, f8, f8, f8, f8)
+    (offs, dx_edge, D_edge, face_mu, face_off, v_off, v_cells, v_b, v_dx, v_sp, v_D) = [
+        np.ascontiguousarray(a, dtype=k) for a, k in zip(packed, kinds)]
+    if face_mu.size == 0:
+        face_mu = np.zeros(1)
+    rho = np.array(rho, dtype=np.float64, copy=True)
+    neg = lib().orc_fvm_steps(_ptr(rho), rho.shape[0], int(n_steps), float(dt), _ptr(offs),
+                              dx_edge.shape[0], _ptr(dx_edge), _ptr(D_edge), _ptr(face_mu),
+                              _ptr(face_off), _ptr(v_off), v_off.shape[0] - 1, _ptr(v_cells),
+                              _ptr(v_b), _ptr(v_dx), _ptr(v_sp), _ptr(v_D), float(neg_floor))
+    return rho, int(neg)

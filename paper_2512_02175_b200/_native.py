@@ -98,7 +98,7 @@ EXPORTS = (
     "gsde_vertex_trials", "gsde_step_batch", "gsde_histogram", "gsde_raw64", "gsde_uniform01",
     "gsde_normal", "gsde_solve_first_passage_s", "gsde_launch_count", "gsde_abi_version",
     "gsde_last_error", "gsde_parse_graph_text", "gsde_parsed_sizes", "gsde_parsed_export",
-    "gsde_parsed_free",
+    "gsde_parsed_free", "gsde_fvm_run",
 )
 
 _lib = None
@@ -125,6 +125,7 @@ def lib():
                 L.gsde_vertex_trials.argtypes = [_P, C.POINTER(Trials), C.POINTER(TrialsOut), _P]
                 L.gsde_step_batch.argtypes = [_P, C.POINTER(StepArgs), _P, _P, _P, _P, _P, _P]
                 L.gsde_histogram.argtypes = [_i64, _P, _P, _P, _P, _P, _i64, _P, _P]
+                L.gsde_fvm_run.argtypes = [_P, _P, _P, _i64, _f64, _f64, _P, _P, _P]
                 L.gsde_raw64.argtypes = [_u64, _u64, _u64]
                 L.gsde_raw64.restype = _u64
                 for name in ("gsde_uniform01", "gsde_normal"):

@@ -54,6 +54,11 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
                                    cudaStream_t s);
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
                                  const gsde_trials_out &o, cudaStream_t s);
+// gsde_fvm.cu (finite-volume baseline; strict IEEE, no FMA contraction)
+cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int64_t n_steps,
+                       double dt, double neg_floor, int64_t *neg_step, uint64_t *red,
+                       cudaStream_t s);
+
 cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,
                              const int64_t *offsets, const int64_t *counts, const double *dx,
                              int64_t n_cells, int64_t *hist, cudaStream_t s);

@@ -1,0 +1,350 @@
+"""Finite-volume Fokker-Planck baseline (reference ``graphsde/fvm.py``), stepped on the GPU.
+
+The density on each edge evolves under ``d(rho)/dt = -dF/dx`` with
+``F = mu rho - D d(rho)/dx``, ``D = sigma^2 / 2``: upwind drift and central
+diffusion on interior faces, explicit Euler in time, and at every vertex of
+degree >= 2 a pairwise, jump-weight-normalised mass exchange between the
+vertex-adjacent cells (``fvm.py:1-27`` states the scheme).
+
+``fvm_run`` packs the static per-face / per-slot coefficients exactly like
+``_pack_static`` (``fvm.py:343-382``), uploads them once and runs every step
+in ONE persistent cooperative kernel (``csrc/gsde_fvm.cu`` via
+``gsde_fvm_run``) that reproduces ``_fvm_step_loop``'s floating-point
+operation order, so the density is bit-identical to the reference's.
+The diagnostic helpers (``fvm_interior_fluxes``, ``fvm_vertex_fluxes``,
+``stability_limit``) are host-side numpy restatements.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .coefficients import CoefficientField, ConstantDrift, LinearDrift, eval_diffusion, eval_drift
+from .graph import AT_INIT, MetricGraph
+from .grids import EdgeGrid
+
+#: Relative negative-density threshold that flags a blown-up solution (``fvm.py:41``).
+_NEGATIVE_TOL = 1e-10
+
+
+class UnstableTimestep(RuntimeError):
+    pass
+
+
+class NegativeDensity(RuntimeError):
+    pass
+
+
+class ZeroJumpWeightAtVertex(ValueError):
+    pass
+
+
+@dataclass
+class FvmState:
+    """Flat per-cell densities (probability per unit length) on a grid (``fvm.py:59-89``)."""
+
+    grid: EdgeGrid
+    rho: np.ndarray
+    t: float = 0.0
+
+    @classmethod
+    def uniform(cls, grid: EdgeGrid, mass: float = 1.0) -> "FvmState":
+        total_len = float(grid.lengths.sum())
+        return cls(grid=grid, rho=np.full(grid.n_cells, mass / total_len, dtype=np.float64), t=0.0)
+
+    @classmethod
+    def from_function(cls, grid: EdgeGrid, f) -> "FvmState":
+        """Sample ``f(edge, x_center)`` on cell centers (no normalization)."""
+        rho = np.empty(grid.n_cells, dtype=np.float64)
+        for e in range(grid.n_edges):
+            rho[grid.edge_slice(e)] = [f(e, float(x)) for x in grid.centers(e)]
+        return cls(grid=grid, rho=rho, t=0.0)
+
+    def mass(self) -> float:
+        return float(np.dot(self.rho, self.grid.cell_widths()))
+
+    def edge_density(self, e: int) -> np.ndarray:
+        return self.rho[self.grid.edge_slice(e)]
+
+    def copy(self) -> "FvmState":
+        return FvmState(grid=self.grid, rho=self.rho.copy(), t=self.t)
+
+
+@dataclass(frozen=True)
+class FvmResult:
+    state: FvmState
+    max_cfl: float
+    n_steps: int
+
+
+def _drift_at(field: CoefficientField, e: int, xs: np.ndarray) -> np.ndarray:
+    """``eval_drift`` on an array of positions (same IEEE results as the scalar calls)."""
+    spec = field.drift[e]
+    if isinstance(spec, ConstantDrift):
+        return np.full(xs.shape, spec.c, dtype=np.float64)
+    if isinstance(spec, LinearDrift):
+        return spec.c * xs
+    return np.interp(xs, spec.xs, spec.mus).astype(np.float64)
+
+
+def _face_drift(field: CoefficientField, e: int, grid: EdgeGrid) -> np.ndarray:
+    """Drift on the interior faces of edge e (``fvm.py:99-103``)."""
+    return _drift_at(field, e, np.arange(1, int(grid.counts[e])) * grid.dx[e])
+
+
+def fvm_interior_fluxes(state: FvmState, field: CoefficientField, grid: EdgeGrid):
+    """Per-edge interior face fluxes ``mu rho_upwind - D (rho_r - rho_l) / dx``
+    (``fvm.py:106-123``)."""
+    out = []
+    for e in range(grid.n_edges):
+        rho = state.edge_density(e)
+        dx = float(grid.dx[e])
+        mu = _face_drift(field, e, grid)
+        D = 0.5 * eval_diffusion(field, e, 0.0) ** 2
+        left, right = rho[:-1], rho[1:]
+        out.append(np.where(mu > 0.0, mu * left, mu * right) + (-D * (right - left) / dx))
+    return out
+
+
+def _vertex_slots(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid, v: int):
+    """``(cells, b, dx, speed_in, D)`` over the incident slots of v (``fvm.py:126-152``)."""
+    inc = graph.incidence[v]
+    offs = grid.offsets
+    deg = inc.degree
+    cells = np.empty(deg, dtype=np.int64)
+    dxs, speed_in, D_v = np.empty(deg), np.empty(deg), np.empty(deg)
+    for i, (eid, orient) in enumerate(zip(inc.edges, inc.orientations)):
+        eid = int(eid)
+        if orient == AT_INIT:
+            cells[i], x_v = offs[eid], 0.0
+        else:
+            cells[i], x_v = offs[eid + 1] - 1, float(grid.lengths[eid])
+        mu = eval_drift(field, eid, x_v)
+        speed_in[i] = max(0.0, -mu if orient == AT_INIT else mu)
+        D_v[i] = 0.5 * eval_diffusion(field, eid, x_v) ** 2
+        dxs[i] = grid.dx[eid]
+    return cells, inc.jump_weights.astype(np.float64), dxs, speed_in, D_v
+
+
+def _zero_weight(v):
+    return ZeroJumpWeightAtVertex(
+        f"vertex {v}: the rho/b normalization needs strictly positive jump weights")
+
+
+def fvm_vertex_fluxes(state: FvmState, field: CoefficientField, graph: MetricGraph,
+                      grid: EdgeGrid, v: int):
+    """``(net, drift_pairs, diff_pairs)`` of the exchange at v (``fvm.py:155-206``)."""
+    inc = graph.incidence[v]
+    deg = inc.degree
+    drift_pairs = np.zeros((deg, deg))
+    diff_pairs = np.zeros((deg, deg))
+    if deg < 2:
+        return np.zeros(deg), drift_pairs, diff_pairs
+    if np.any(inc.jump_weights <= 0.0):
+        raise _zero_weight(v)
+    cells, b, dxs, speed_in, D_v = _vertex_slots(graph, field, grid, v)
+    rho = state.rho[cells]
+    conc = rho / b
+    for i in range(deg):
+        others = 1.0 - b[i]
+        if speed_in[i] <= 0.0 or others <= 0.0:
+            continue
+        total = speed_in[i] * rho[i]
+        for j in range(deg):
+            if j != i:
+                drift_pairs[i, j] = total * b[j] / others
+    for i in range(deg):
+        for j in range(i + 1, deg):
+            dpair = 0.5 * (D_v[i] + D_v[j])
+            dxh = 2.0 * dxs[i] * dxs[j] / (dxs[i] + dxs[j])
+            g = dpair * (conc[i] - conc[j]) / dxh
+            if g >= 0.0:
+                diff_pairs[i, j] = g * b[j]
+            else:
+                diff_pairs[j, i] = -g * b[i]
+    flows = drift_pairs + diff_pairs
+    return flows.sum(axis=0) - flows.sum(axis=1), drift_pairs, diff_pairs
+
+
+@dataclass(frozen=True)
+class _Packed:
+    """``_pack_static`` (``fvm.py:343-382``) + the GPU's ownership split."""
+
+    offs: np.ndarray
+    dx_edge: np.ndarray
+    D_edge: np.ndarray
+    face_mu: np.ndarray
+    face_off: np.ndarray
+    v_off: np.ndarray
+    v_cells: np.ndarray
+    v_b: np.ndarray
+    v_dx: np.ndarray
+    v_speed_in: np.ndarray
+    v_D: np.ndarray
+    cell_edge: np.ndarray
+    owned: np.ndarray
+    vpar: np.ndarray
+    vser: np.ndarray
+
+    def reference_tuple(self):
+        return (self.offs, self.dx_edge, self.D_edge, self.face_mu, self.face_off, self.v_off,
+                self.v_cells, self.v_b, self.v_dx, self.v_speed_in, self.v_D)
+
+
+def _pack(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> _Packed:
+    E = grid.n_edges
+    counts = np.asarray(grid.counts, np.int64)
+    offs = grid.offsets
+    dx = np.asarray(grid.dx, np.float64)
+    faces = [_face_drift(field, e, grid) for e in range(E)]
+    face_off = np.zeros(E + 1, dtype=np.int64)
+    np.cumsum(np.maximum(counts - 1, 0), out=face_off[1:])
+    face_mu = np.concatenate(faces) if face_off[-1] else np.zeros(0, dtype=np.float64)
+    sig = np.array([eval_diffusion(field, e, 0.0) for e in range(E)], dtype=np.float64)
+    D_edge = 0.5 * sig ** 2
+    # vertex slots, vectorised over the graph's CSR (slot order = incidence order)
+    v_off = np.asarray(graph.v_off, np.int64).copy()
+    ve = np.asarray(graph.v_edges, np.int64)
+    at_init = np.asarray(graph.v_orient) == AT_INIT
+    v_cells = np.where(at_init, offs[ve], offs[ve + 1] - 1).astype(np.int64)
+    x_v = np.where(at_init, 0.0, np.asarray(grid.lengths, np.float64)[ve])
+    mu_v = np.empty(ve.shape[0])
+    for e in np.unique(ve):
+        sel = ve == e
+        mu_v[sel] = _drift_at(field, int(e), x_v[sel])
+    speed = np.where(at_init, -mu_v, mu_v)
+    v_speed_in = np.where(speed > 0.0, speed, 0.0)
+    v_D = 0.5 * sig[ve] ** 2
+    v_b = np.asarray(graph.v_weights, np.float64).copy()
+    v_dx = dx[ve]
+    deg = np.diff(v_off)
+    slot_vertex = np.repeat(np.arange(deg.shape[0], dtype=np.int64), deg)
+    multi = deg[slot_vertex] >= 2
+    bad = np.unique(slot_vertex[multi & (v_b <= 0.0)])
+    if bad.size:
+        raise _zero_weight(int(bad[0]))
+    n_cells = int(counts.sum())
+    owners = np.bincount(v_cells[multi], minlength=n_cells)
+    shared = np.zeros(deg.shape[0], dtype=bool)
+    shared[np.unique(slot_vertex[multi & (owners[v_cells] >= 2)])] = True
+    hub = deg >= 2
+    return _Packed(
+        offs=offs, dx_edge=dx, D_edge=D_edge, face_mu=face_mu, face_off=face_off, v_off=v_off,
+        v_cells=v_cells, v_b=v_b, v_dx=v_dx, v_speed_in=v_speed_in, v_D=v_D,
+        cell_edge=np.repeat(np.arange(E, dtype=np.int64), counts),
+        owned=(owners >= 1).astype(np.uint8),
+        vpar=np.flatnonzero(hub & ~shared).astype(np.int64),
+        vser=np.flatnonzero(hub & shared).astype(np.int64))
+
+
+def stability_limit(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> float:
+    """Largest dt the explicit stepper accepts, CFL = 1 (``fvm.py:209-251``),
+    vectorised with the reference's per-element arithmetic and summation order."""
+    max_rate = 0.0
+    for e in range(grid.n_edges):
+        dx = float(grid.dx[e])
+        xs = np.arange(int(grid.counts[e]) + 1) * dx
+        mu_max = float(np.max(np.abs(_drift_at(field, e, xs))))
+        D = 0.5 * eval_diffusion(field, e, 0.0) ** 2
+        max_rate = max(max_rate, mu_max / dx + 2.0 * D / (dx * dx))
+    p = _pack(graph, field, grid)
+    deg = np.diff(p.v_off)
+    for v in np.flatnonzero(deg >= 2):
+        lo, hi = int(p.v_off[v]), int(p.v_off[v + 1])
+        b, dxs, D_v = p.v_b[lo:hi], p.v_dx[lo:hi], p.v_D[lo:hi]
+        for i in range(hi - lo):
+            diff_rate = 0.0
+            for j in range(hi - lo):
+                if j == i:
+                    continue
+                dxh = 2.0 * dxs[i] * dxs[j] / (dxs[i] + dxs[j])
+                diff_rate += D_v[i] * b[j] / (b[i] * dxh)
+            dx = float(dxs[i])
+            eid = int(graph.v_edges[lo + i])
+            x_v = 0.0 if graph.v_orient[lo + i] == AT_INIT else float(grid.lengths[eid])
+            mu_abs = abs(eval_drift(field, eid, x_v))
+            rate = (p.v_speed_in[lo + i] / dx + diff_rate / dx + mu_abs / dx
+                    + 2.0 * D_v[i] / (dx * dx))
+            max_rate = max(max_rate, rate)
+    if max_rate == 0.0:
+        return math.inf
+    return 1.0 / max_rate
+
+
+class _Desc(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n_edges", "n_cells", "n_vertices", "n_vpar", "n_vser")] + [
+        (n, C.c_void_p) for n in ("offs", "dx_edge", "D_edge", "face_mu", "face_off", "v_off",
+                                  "v_cells", "v_b", "v_dx", "v_speed_in", "v_D", "cell_edge",
+                                  "owned", "vpar", "vser")]
+
+
+def _device_pack(p: _Packed, n_vertices: int, device: int):
+    torch, dev = _native.torch_cuda(device)
+    kw = dict(device=f"cuda:{dev}")
+    keep = {}
+    d = _Desc()
+    d.n_edges, d.n_cells = p.dx_edge.shape[0], p.cell_edge.shape[0]
+    d.n_vertices, d.n_vpar, d.n_vser = n_vertices, p.vpar.shape[0], p.vser.shape[0]
+    for name in ("offs", "dx_edge", "D_edge", "face_mu", "face_off", "v_off", "v_cells", "v_b",
+                 "v_dx", "v_speed_in", "v_D", "cell_edge", "owned", "vpar", "vser"):
+        a = getattr(p, name)
+        t = torch.from_numpy(np.ascontiguousarray(a) if a.size else np.zeros(1, a.dtype)).to(**kw)
+        keep[name] = t
+        setattr(d, name, t.data_ptr())
+    return d, keep, torch, dev
+
+
+def fvm_run(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid, dt: float,
+            n_steps: int, initial: FvmState, force: bool = False) -> FvmResult:
+    """Advance the density ``n_steps`` explicit Euler steps of size ``dt`` (``fvm.py:385-422``).
+
+    Raises :class:`UnstableTimestep` when the predicted CFL number exceeds 1
+    unless ``force``; a developing negative density raises
+    :class:`NegativeDensity`.  The steps run on the GPU (bit-identical to the
+    reference stepper)."""
+    if not dt > 0.0:
+        raise ValueError(f"dt must be positive, got {dt!r}")
+    if not initial.grid.same_geometry(grid):
+        raise ValueError("initial state lives on a different grid")
+    limit = stability_limit(graph, field, grid)
+    max_cfl = dt / limit if math.isfinite(limit) else 0.0
+    if max_cfl > 1.0 and not force:
+        raise UnstableTimestep(
+            f"dt={dt:g} exceeds the stability limit {limit:g} (CFL={max_cfl:.3g}); "
+            "pass force=True to run anyway")
+    state = initial.copy()
+    rho, neg = fvm_steps_device(graph, field, grid, state.rho, int(n_steps), float(dt))
+    state.rho = rho
+    if neg:
+        state.t += neg * dt
+        raise NegativeDensity(
+            f"density went negative at t={state.t:g} (step {neg}); the timestep is unstable")
+    state.t += n_steps * dt
+    return FvmResult(state=state, max_cfl=max_cfl, n_steps=int(n_steps))
+
+
+def fvm_steps_device(graph, field, grid, rho, n_steps, dt, device=None, stream=None):
+    """The stepper alone (no CFL check): returns (rho after the run, 1-based
+    negative step or 0).  ``rho`` may be a numpy array (copied to and from the
+    device) or a CUDA float64 tensor (updated in place)."""
+    p = _pack(graph, field, grid)
+    d, keep, torch, dev = _device_pack(p, graph.n_vertices, device)
+    host = not (hasattr(rho, "is_cuda") and rho.is_cuda)
+    r = (torch.from_numpy(np.array(rho, dtype=np.float64, copy=True)).to(f"cuda:{dev}")
+         if host else rho)
+    if r.dtype != torch.float64 or r.numel() != p.cell_edge.shape[0]:
+        raise ValueError("rho must be float64 with one value per grid cell")
+    scratch = torch.empty_like(r)
+    neg = torch.zeros(1, dtype=torch.int64, device=r.device)
+    red = torch.zeros(8, dtype=torch.int64, device=r.device)
+    s = stream if stream is not None else _native.cur_stream(dev)
+    _native.check(_native.lib().gsde_fvm_run(C.byref(d), r.data_ptr(), scratch.data_ptr(),
+                                             int(n_steps), float(dt), -_NEGATIVE_TOL,
+                                             neg.data_ptr(), red.data_ptr(), s))
+    n = int(neg.item())
+    return (r.cpu().numpy() if host else r), n

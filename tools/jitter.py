@@ -16,4 +16,5 @@ for _ in range(n):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s); r = wl.launch(s.cuda_stream); b.record(s); ev.append((a, b, r))
 torch.cuda.synchronize()
-print(w, [round(a.elapsed_time(b), 2) for a, b, _ in ev])
+ms = [round(a.elapsed_time(b), 2) for a, b, _ in ev]
+print(w, "min %.2f ms" % min(ms), "-> %.4g %s" % (wl.units_per_step / min(ms) * 1e3, wl.unit), ms)
