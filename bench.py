@@ -115,27 +115,36 @@ class Ensemble(Workload):
 
 
 class Trials(Workload):
+    """C3: the dt-convergence sweep of exit_probability_experiment (analysis.py:348-384):
+    vertex trials at dt = 1e-2 .. 1e-5 (seed + i per dt, like the reference), fused exit
+    counts + M histogram; one launch per dt."""
+
     unit = "trials/s"
 
-    def __init__(self, rank=0, world=1, n_per_gpu=250_000_000, dt=1e-3):
+    def __init__(self, rank=0, world=1, n_per_dt=1_000_000_000,
+                 dts=(1e-2, 1e-3, 1e-4, 1e-5)):
         super().__init__(rank, world)
         from paper_2512_02175_b200 import workloads
 
         self.name = "star5_trials"
-        self.desc = ("C3: paper §4.1 5-edge star, ConstantDrift(-10 i), vertex trials at "
-                     f"dt={dt} (fused exit counts + M histogram)")
+        self.desc = ("C3: paper §4.1 5-edge star, ConstantDrift(-10 i), dt sweep "
+                     f"{', '.join(f'{d:g}' for d in dts)} x {n_per_dt:.0e} vertex trials per "
+                     "GPU each (fused exit counts + M histogram)")
         self.g, self.f = workloads.star5("linear")
-        self.n, self.dt = n_per_gpu, dt
-        self.units_per_step = n_per_gpu
+        self.n, self.dts = n_per_dt, tuple(dts)
+        self.units_per_step = n_per_dt * len(dts)
 
     def config(self):
-        return {"workload": self.desc, "n_trials_per_gpu": self.n, "dt": self.dt}
+        return {"workload": self.desc, "n_trials_per_dt_per_gpu": self.n, "dts": list(self.dts)}
 
     def launch(self, stream):
+        import torch
         from paper_2512_02175_b200 import engine
 
-        return engine.trials_device(self.g, self.f, self.dt, self.n, 11, per_trial=False,
-                                    trial_offset=self.rank * self.n, stream=stream)
+        parts = [engine.trials_device(self.g, self.f, dt, self.n, 11 + i, per_trial=False,
+                                      trial_offset=self.rank * self.n, stream=stream)
+                 for i, dt in enumerate(self.dts)]
+        return {k: torch.cat([p[k] for p in parts]) for k in ("exit_counts", "m_hist", "totals")}
 
     def reduce_tensor(self, res):
         import torch
@@ -143,7 +152,56 @@ class Trials(Workload):
         return torch.cat([res["exit_counts"], res["m_hist"], res["totals"]])
 
     def crossings(self, res):
-        return int(res["totals"][0])
+        return int(res["totals"].view(-1, 4)[:, 0].sum())
+
+
+class FvmWork(Workload):
+    """Finite-volume baseline on the C4 network: 8 cells per edge,
+    dt = 0.9 x the stability limit, 2000 explicit steps per bench step, one launch."""
+
+    unit = "cell-steps/s"
+
+    def __init__(self, rank=0, world=1, cells=8, n_steps=2000):
+        super().__init__(rank, world)
+        import paper_2512_02175_b200 as gs
+        import torch
+        from paper_2512_02175_b200 import fvm
+
+        self.name = "fvm_vascular"
+        self.g, self.f = _vascular_cached()
+        self.grid = gs.EdgeGrid.uniform(self.g, cells)
+        self.dt = 0.9 * fvm.stability_limit(self.g, self.f, self.grid)
+        self.n_steps = n_steps
+        self.fd = fvm.FvmDevice(self.g, self.f, self.grid, torch.cuda.current_device())
+        self.rho0 = torch.tensor(fvm.FvmState.uniform(self.grid).rho, device="cuda")
+        self.rho = self.rho0.clone()
+        self.units_per_step = self.grid.n_cells * n_steps
+        self.desc = (f"FVM baseline (fvm_run) on the C4 network: {self.g.n_edges} edges x "
+                     f"{cells} cells, dt = 0.9 x stability limit, {n_steps} steps per launch")
+
+    def config(self):
+        return {"workload": self.desc, "n_cells": self.grid.n_cells, "n_steps": self.n_steps,
+                "dt": self.dt}
+
+    def launch(self, stream):
+        self.rho.copy_(self.rho0)
+        return {"neg": self.fd.run(self.rho, self.n_steps, self.dt, stream)}
+
+    def reduce_tensor(self, res):
+        return res["neg"]
+
+    def crossings(self, res):
+        return 0
+
+    def cpu_rate(self, steps=10):
+        """Single-thread C restatement of the reference stepper (the reference
+        is single-threaded by design, fvm.py:25-28): cell-steps/s."""
+        from oracle import oracle
+
+        rho = self.rho0.cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.fvm_steps(rho, steps, self.dt, self.fd.packed.reference_tuple())
+        return self.grid.n_cells * steps / (time.perf_counter() - t0)
 
 
 def make_workload(name, rank, world):
@@ -153,7 +211,8 @@ def make_workload(name, rank, world):
     if name == "star3":
         return Ensemble(
             "star3", "C1-throughput: 3-edge star, Brownian (mu=0, sigma=1), AtVertex(0), "
-            "dt=1e-3, 1000 steps, 1.6e7 particles/GPU; fused 3x16-cell histogram + occupancy",
+            "dt=1e-3, 1000 steps, 1.6e7 particles/GPU; fused 3x16-cell snapshot histogram + "
+            "final-edge counts",
             workloads.star3, 16_000_000, 1000, 1e-3, lambda g: gs.AtVertex(0),
             lambda g: gs.EdgeGrid.uniform(g, 16, lengths=[3.0] * 3), rank, world)
     if name == "hub64":
@@ -172,6 +231,8 @@ def make_workload(name, rank, world):
             lambda g: gs.EdgeGrid.uniform(g, 8), rank, world)
     if name == "star5_trials":
         return Trials(rank, world)
+    if name == "fvm":
+        return FvmWork(rank, world)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -271,6 +332,12 @@ class ClockSampler:
 
 def flush_l2(buf):
     buf.fill_(1)  # 256 MiB write > 126 MB L2
+
+
+# FVM step, algorithmic bytes per cell: read rho[c] (8) + the face drift shared
+# with the neighbour (8) + cell->edge (8) + owned flag (1), write new[c] (8);
+# neighbour densities and per-edge constants are L1 hits.
+FVM_BYTES_PER_CELL_STEP = 33
 
 
 def lane_ops_per_pstep(crossings_per_pstep):
@@ -434,7 +501,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="star3",
-                    choices=["star3", "hub64", "star5_trials", "vascular"])
+                    choices=["star3", "hub64", "star5_trials", "vascular", "fvm"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -527,13 +594,26 @@ def main():
             line["cpu_baseline"] = cpu_baseline(wl)
         if not args.no_extras and world == 1:
             extras = {}
-            for name in ("hub64", "star5_trials", "vascular"):
+            for name in ("hub64", "star5_trials", "vascular", "fvm"):
                 if name == args.workload:
                     continue
                 w2 = make_workload(name, 0, 1)
                 t2, k2, r2, _, _ = time_workload(w2, 2, 1, None, torch, dev, flush_buf)
-                c2 = w2.crossings(r2) / w2.units_per_step
                 rate2 = w2.units_per_step * 2 / t2
+                if name == "fvm":
+                    bpc = FVM_BYTES_PER_CELL_STEP
+                    extras[name] = {
+                        "value": rate2, "unit": w2.unit, "config": w2.config(),
+                        "bytes_per_cell_step": bpc, "achieved_gbs": rate2 * bpc / 1e9,
+                        "frac_of_hbm_peak": rate2 * bpc / 1e9 / float(peaks.get("hbm_gbs", 7700)),
+                        "note": "working set (~40 MB) is L2-resident across steps",
+                        "cpu_baseline": {"value": w2.cpu_rate(), "unit": w2.unit, "cores": 1,
+                                         "kind": "port",
+                                         "sample": "10 steps, oracle/gsde_oracle.c "
+                                                   "orc_fvm_steps (single thread, like the "
+                                                   "reference)"}}
+                    continue
+                c2 = w2.crossings(r2) / w2.units_per_step
                 extras[name] = {"value": rate2, "unit": w2.unit, "config": w2.config(),
                                 "crossings_per_unit": c2,
                                 "roofline_frac": rate2 * lane_ops_per_pstep(c2) / peak_ops}

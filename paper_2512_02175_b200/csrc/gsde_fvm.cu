@@ -59,43 +59,58 @@ struct Fvm {
     return v;
   }
 
-  // vertex exchange at v (fvm.py:305-328) applied to out[] (cells owned here)
-  __device__ void vertex(int64_t v) const {
-    const int64_t lo = d.v_off[v], hi = d.v_off[v + 1];
-    if (hi - lo < 2) return;
-    for (int64_t i = lo; i < hi; ++i) {
-      const int64_t ci = d.v_cells[i];
-      const double bi = d.v_b[i];
-      const double rho_i = rho[ci];
-      if (d.v_speed_in[i] > 0.0) {
+  // vertex exchange at v (fvm.py:305-328) applied to out[] (cells owned here),
+  // through accessors so the same loop runs on registers/local memory (small
+  // degree) or directly on global memory (hubs, shared cells)
+  template <class Nw, class Rho, class B, class Dx, class Sp, class Dv>
+  __device__ __forceinline__ void exchange(int n, Nw &&nw, Rho &&r, B &&b, Dx &&dx, Sp &&sp,
+                                           Dv &&Dd) const {
+    for (int i = 0; i < n; ++i) {
+      const double bi = b(i);
+      const double rho_i = r(i);
+      if (sp(i) > 0.0) {
         const double others = 1.0 - bi;
         if (others > 0.0) {
-          const double total = d.v_speed_in[i] * rho_i;
-          for (int64_t j = lo; j < hi; ++j) {
+          const double total = sp(i) * rho_i;
+          for (int j = 0; j < n; ++j) {
             if (j == i) continue;
-            const double f = total * d.v_b[j] / others;
-            out[d.v_cells[j]] += dt * f / d.v_dx[j];
-            out[ci] -= dt * f / d.v_dx[i];
+            const double f = total * b(j) / others;
+            nw(j) += dt * f / dx(j);
+            nw(i) -= dt * f / dx(i);
           }
         }
       }
       const double conc_i = rho_i / bi;
-      for (int64_t j = i + 1; j < hi; ++j) {
-        const int64_t cj = d.v_cells[j];
-        const double dpair = 0.5 * (d.v_D[i] + d.v_D[j]);
-        const double dxh = 2.0 * d.v_dx[i] * d.v_dx[j] / (d.v_dx[i] + d.v_dx[j]);
-        const double g = dpair * (conc_i - rho[cj] / d.v_b[j]) / dxh;
+      for (int j = i + 1; j < n; ++j) {
+        const double dpair = 0.5 * (Dd(i) + Dd(j));
+        const double dxh = 2.0 * dx(i) * dx(j) / (dx(i) + dx(j));
+        const double g = dpair * (conc_i - r(j) / b(j)) / dxh;
         if (g >= 0.0) {
-          const double f = g * d.v_b[j];
-          out[cj] += dt * f / d.v_dx[j];
-          out[ci] -= dt * f / d.v_dx[i];
+          const double f = g * b(j);
+          nw(j) += dt * f / dx(j);
+          nw(i) -= dt * f / dx(i);
         } else {
-          const double f = -g * d.v_b[i];
-          out[ci] += dt * f / d.v_dx[i];
-          out[cj] -= dt * f / d.v_dx[j];
+          const double f = -g * b(i);
+          nw(i) += dt * f / dx(i);
+          nw(j) -= dt * f / dx(j);
         }
       }
     }
+  }
+
+  // whole update of a vertex whose cells no other vertex touches: face terms
+  // then exchange, slot values staged in local arrays (L1) for degree <= 8
+  __device__ void vertex_private(int64_t v, double &amax, double &nmin) const;
+
+  // exchange on global memory, in place on out[] (cells already initialised)
+  __device__ void vertex(int64_t v) const {
+    const int64_t lo = d.v_off[v], hi = d.v_off[v + 1];
+    if (hi - lo < 2) return;
+    const int64_t *cell = d.v_cells + lo;
+    exchange((int)(hi - lo), [&](int k) -> double & { return out[cell[k]]; },
+             [&](int k) { return rho[cell[k]]; }, [&](int k) { return d.v_b[lo + k]; },
+             [&](int k) { return d.v_dx[lo + k]; }, [&](int k) { return d.v_speed_in[lo + k]; },
+             [&](int k) { return d.v_D[lo + k]; });
   }
 
   __device__ __forceinline__ void init_cells(int64_t v) const {
@@ -106,6 +121,37 @@ struct Fvm {
 __device__ __forceinline__ void track(double v, double &amax, double &nmin) {
   amax = fmax(amax, fabs(v));
   nmin = fmax(nmin, -v);
+}
+
+constexpr int kLocalDeg = 8;
+
+__device__ void Fvm::vertex_private(int64_t v, double &amax, double &nmin) const {
+  const int64_t lo = d.v_off[v], hi = d.v_off[v + 1];
+  const int n = (int)(hi - lo);
+  if (n > kLocalDeg) {
+    init_cells(v);
+    vertex(v);
+    for (int64_t i = lo; i < hi; ++i) track(out[d.v_cells[i]], amax, nmin);
+    return;
+  }
+  double nw[kLocalDeg], r[kLocalDeg], b[kLocalDeg], dx[kLocalDeg], sp[kLocalDeg], Dd[kLocalDeg];
+  int64_t cell[kLocalDeg];
+  for (int k = 0; k < n; ++k) {
+    cell[k] = d.v_cells[lo + k];
+    nw[k] = base(cell[k]);
+    r[k] = rho[cell[k]];
+    b[k] = d.v_b[lo + k];
+    dx[k] = d.v_dx[lo + k];
+    sp[k] = d.v_speed_in[lo + k];
+    Dd[k] = d.v_D[lo + k];
+  }
+  exchange(n, [&](int k) -> double & { return nw[k]; }, [&](int k) { return r[k]; },
+           [&](int k) { return b[k]; }, [&](int k) { return dx[k]; },
+           [&](int k) { return sp[k]; }, [&](int k) { return Dd[k]; });
+  for (int k = 0; k < n; ++k) {
+    out[cell[k]] = nw[k];
+    track(nw[k], amax, nmin);
+  }
 }
 
 __global__ void __launch_bounds__(kFvmThreads)
@@ -129,10 +175,7 @@ __global__ void __launch_bounds__(kFvmThreads)
         f.out[it] = v;
         track(v, amax, nmin);
       } else if (it < d.n_cells + d.n_vpar) {
-        const int64_t v = d.vpar[it - d.n_cells];
-        f.init_cells(v);
-        f.vertex(v);
-        for (int64_t i = d.v_off[v]; i < d.v_off[v + 1]; ++i) track(f.out[d.v_cells[i]], amax, nmin);
+        f.vertex_private(d.vpar[it - d.n_cells], amax, nmin);
       } else {
         for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
         for (int64_t k = 0; k < d.n_vser; ++k) f.vertex(d.vser[k]);

@@ -328,23 +328,41 @@ def fvm_run(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid, dt: flo
     return FvmResult(state=state, max_cfl=max_cfl, n_steps=int(n_steps))
 
 
+class FvmDevice:
+    """A (graph, field, grid) packed and resident on one GPU; ``run`` steps a
+    device density in place (the whole run is one kernel launch)."""
+
+    def __init__(self, graph, field, grid, device=None):
+        self.packed = _pack(graph, field, grid)
+        self.desc, self._keep, self.torch, self.device = _device_pack(
+            self.packed, graph.n_vertices, device)
+        self.n_cells = self.packed.cell_edge.shape[0]
+        t = self.torch
+        self._scratch = t.empty(self.n_cells, dtype=t.float64, device=f"cuda:{self.device}")
+        self._red = t.zeros(8, dtype=t.int64, device=f"cuda:{self.device}")
+
+    def run(self, rho, n_steps: int, dt: float, stream=None):
+        """Advance the device tensor ``rho`` in place; returns a device int64[1]
+        holding the 1-based negative-density step (0 = none)."""
+        t = self.torch
+        if rho.dtype != t.float64 or rho.numel() != self.n_cells or not rho.is_contiguous():
+            raise ValueError("rho must be a contiguous float64 tensor with one value per cell")
+        neg = t.zeros(1, dtype=t.int64, device=rho.device)
+        s = stream if stream is not None else _native.cur_stream(self.device)
+        _native.check(_native.lib().gsde_fvm_run(
+            C.byref(self.desc), rho.data_ptr(), self._scratch.data_ptr(), int(n_steps), float(dt),
+            -_NEGATIVE_TOL, neg.data_ptr(), self._red.data_ptr(), s))
+        return neg
+
+
 def fvm_steps_device(graph, field, grid, rho, n_steps, dt, device=None, stream=None):
     """The stepper alone (no CFL check): returns (rho after the run, 1-based
     negative step or 0).  ``rho`` may be a numpy array (copied to and from the
     device) or a CUDA float64 tensor (updated in place)."""
-    p = _pack(graph, field, grid)
-    d, keep, torch, dev = _device_pack(p, graph.n_vertices, device)
+    fd = FvmDevice(graph, field, grid, device)
+    torch = fd.torch
     host = not (hasattr(rho, "is_cuda") and rho.is_cuda)
-    r = (torch.from_numpy(np.array(rho, dtype=np.float64, copy=True)).to(f"cuda:{dev}")
+    r = (torch.from_numpy(np.array(rho, dtype=np.float64, copy=True)).to(f"cuda:{fd.device}")
          if host else rho)
-    if r.dtype != torch.float64 or r.numel() != p.cell_edge.shape[0]:
-        raise ValueError("rho must be float64 with one value per grid cell")
-    scratch = torch.empty_like(r)
-    neg = torch.zeros(1, dtype=torch.int64, device=r.device)
-    red = torch.zeros(8, dtype=torch.int64, device=r.device)
-    s = stream if stream is not None else _native.cur_stream(dev)
-    _native.check(_native.lib().gsde_fvm_run(C.byref(d), r.data_ptr(), scratch.data_ptr(),
-                                             int(n_steps), float(dt), -_NEGATIVE_TOL,
-                                             neg.data_ptr(), red.data_ptr(), s))
-    n = int(neg.item())
+    n = int(fd.run(r, n_steps, dt, stream).item())
     return (r.cpu().numpy() if host else r), n
