@@ -598,8 +598,8 @@ def main():
                 if name == args.workload:
                     continue
                 w2 = make_workload(name, 0, 1)
-                t2, k2, r2, _, _ = time_workload(w2, 2, 1, None, torch, dev, flush_buf)
-                rate2 = w2.units_per_step * 2 / t2
+                t2, k2, r2, _, _ = time_workload(w2, 3, 2, None, torch, dev, flush_buf)
+                rate2 = w2.units_per_step * 3 / t2
                 if name == "fvm":
                     bpc = FVM_BYTES_PER_CELL_STEP
                     extras[name] = {
@@ -615,7 +615,7 @@ def main():
                     continue
                 c2 = w2.crossings(r2) / w2.units_per_step
                 extras[name] = {"value": rate2, "unit": w2.unit, "config": w2.config(),
-                                "crossings_per_unit": c2,
+                                "step_ms": list(STEP_MS), "crossings_per_unit": c2,
                                 "roofline_frac": rate2 * lane_ops_per_pstep(c2) / peak_ops}
             line["workloads"] = extras
         print(json.dumps(line), flush=True)
