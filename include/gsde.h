@@ -190,29 +190,31 @@ int gsde_histogram(int64_t n, const int64_t *edge, const double *x, const int64_
                    void *stream);
 
 /* Finite-volume Fokker-Planck baseline (fvm.py): the packed static arrays of
- * fvm._pack_static (fvm.py:343-382) plus an ownership split of the vertex
- * exchange, all DEVICE pointers.  Vertex v's slots are v_off[v]..v_off[v+1];
- * owned[c] = 1 when cell c is the vertex-adjacent cell of a vertex of degree
- * >= 2 (its update is done by that vertex's thread); vpar lists the vertices
- * whose cells no other vertex touches, vser (ascending) the rest (cells shared
- * through single-cell edges), which one thread processes in vertex order. */
+ * fvm._pack_static (fvm.py:343-382) re-laid per cell, plus an ownership split
+ * of the vertex exchange; all DEVICE pointers.  Cell c of edge e carries the
+ * drift on its left / right interior face, D = sigma_e^2 / 2 and dx_e, and
+ * flags: bit 0 = has a left interior face, bit 1 = has a right one, bit 2 =
+ * vertex-adjacent cell of a vertex of degree >= 2 (that vertex's item
+ * updates it).  Vertex v's slots are v_off[v]..v_off[v+1]; pslot lists the
+ * slots of the vertices whose cells no other vertex touches (one thread per
+ * slot), vser (ascending) the other degree >= 2 vertices (cells shared
+ * through single-cell edges), processed in vertex order by one thread. */
 typedef struct {
-  int64_t n_edges, n_cells, n_vertices, n_vpar, n_vser;
-  const int64_t *offs;       /* [E+1] grid offsets */
-  const double *dx_edge;     /* [E] cell width */
-  const double *D_edge;      /* [E] sigma^2 / 2 */
-  const double *face_mu;     /* [F] drift on interior faces, edge-major */
-  const int64_t *face_off;   /* [E+1] */
+  int64_t n_edges, n_cells, n_vertices, n_pslot, n_vser;
+  const double *cell_mu_l;   /* [C] drift on the left face (0 if none) */
+  const double *cell_mu_r;   /* [C] drift on the right face (0 if none) */
+  const double *cell_D;      /* [C] */
+  const double *cell_dx;     /* [C] */
+  const uint8_t *cell_flags; /* [C] */
   const int64_t *v_off;      /* [V+1] */
   const int64_t *v_cells;    /* [S] vertex-adjacent cell per slot */
   const double *v_b;         /* [S] jump weight */
   const double *v_dx;        /* [S] */
   const double *v_speed_in;  /* [S] inward drift speed (>= 0) */
   const double *v_D;         /* [S] */
-  const int64_t *cell_edge;  /* [C] edge of each cell */
-  const uint8_t *owned;      /* [C] */
-  const int64_t *vpar;       /* [n_vpar] */
-  const int64_t *vser;       /* [n_vser] ascending */
+  const int64_t *slot_vertex; /* [S] vertex of each slot */
+  const int64_t *pslot;      /* [n_pslot] slots of the vertices whose cells no other vertex touches */
+  const int64_t *vser;       /* [n_vser] the other degree >= 2 vertices, ascending */
 } gsde_fvm_desc;
 
 /* fvm_run's stepper (_fvm_step_loop, fvm.py:254-340): n_steps explicit Euler
@@ -221,7 +223,8 @@ typedef struct {
  * FP64).  After each step the run stops if min(0, min rho) <
  * neg_floor * max(1, max |rho|); *neg_step (device int64) receives the
  * 1-based step index, 0 if none.  red: caller-owned device scratch of 8
- * uint64.  One persistent cooperative kernel, one grid barrier per step. */
+ * uint64.  One kernel per step (one thread per cell / vertex slot), all
+ * stream-ordered; the stop test runs in the last block of each step. */
 int gsde_fvm_run(const gsde_fvm_desc *d, double *rho, double *scratch, int64_t n_steps,
                  double dt, double neg_floor, int64_t *neg_step, uint64_t *red, void *stream);
 

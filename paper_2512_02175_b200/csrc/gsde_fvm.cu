@@ -1,67 +1,71 @@
 // gsde_fvm.cu -- finite-volume Fokker-Planck baseline (reference fvm.py) on the GPU.
 //
-// One persistent cooperative kernel runs all explicit Euler steps: per step
-// every work item writes a disjoint set of cells of the next density, then
-// one grid barrier.  Work items:
+// One kernel per explicit Euler step, one thread per work item, every item
+// writing a disjoint set of cells of the next density:
 //   * a cell not adjacent to a degree >= 2 vertex: rho +- its two interior
-//     face fluxes;
-//   * a vertex whose adjacent cells no other vertex touches: its cells'
-//     face terms, then the vertex exchange in the reference's loop order;
+//     face fluxes (per-cell SoA records: face drifts, D, dx -- one level of
+//     independent, coalesced loads);
+//   * a slot of a vertex whose adjacent cells no other vertex touches: the
+//     slot cell's face terms, then the contributions of the vertex exchange
+//     to that cell in the reference's loop order (O(degree) per thread);
 //   * one item for the remaining vertices (cells shared through single-cell
 //     edges): the same, one vertex after another in ascending order.
-// Every cell therefore sees the same sequence of IEEE additions as in
+// Every cell therefore sees the same sequence of IEEE operations as in
 // _fvm_step_loop (fvm.py:254-340): the file is compiled without FMA
-// contraction and results are bit-identical to the reference.  The density
-// (8 B/cell, e.g. 6.5 MB for a 1e5-edge network at 8 cells per edge) stays in
-// L2 across steps; the step is bound by L2 bandwidth and the barrier.
-// The negativity check (fvm.py:330-337) is a per-step max-reduction through
-// 64-bit atomics on the bit patterns of non-negative doubles.
-#include <cooperative_groups.h>
+// contraction and results are bit-identical to the reference.  The state
+// (8 B/cell: 6.5 MB for the 1e5-edge network at 8 cells per edge) stays in L2
+// across steps.  The negativity check (fvm.py:330-337) is a per-step max
+// reduction through 64-bit atomics on the bit patterns of non-negative
+// doubles, evaluated by the step's last block; later step kernels see the
+// stop flag and return at once, so the whole run is enqueued without a host
+// round trip.
 #include <cuda_runtime.h>
 
 #include "gsde_internal.h"
-
-namespace cg = cooperative_groups;
 
 namespace gsde {
 namespace {
 
 constexpr int kFvmThreads = 256;
+enum : uint8_t { kLeft = 1, kRight = 2, kOwned = 4 };
 
+// red[] layout: [0] max |rho|, [1] max(-rho) of the running step (double bit
+// patterns), [2] blocks finished, [3] steps done
 struct Fvm {
   const gsde_fvm_desc &d;
   double dt;
   const double *rho;
   double *out;
 
-  // interior face flux at face j of edge e (between cells j-1 and j), exactly
-  // fvm.py:287-292
-  __device__ __forceinline__ double face(int64_t e, int64_t lo, int64_t j) const {
-    const double mu = d.face_mu[d.face_off[e] + (j - lo - 1)];
+  // interior face flux with drift mu between cells l and r (fvm.py:287-292)
+  __device__ __forceinline__ double face(double mu, double D, double dx, double rl,
+                                         double rr) const {
     double F;
     if (mu > 0.0)
-      F = mu * rho[j - 1];
+      F = mu * rl;
     else
-      F = mu * rho[j];
-    F -= d.D_edge[e] * (rho[j] - rho[j - 1]) / d.dx_edge[e];
+      F = mu * rr;
+    F -= D * (rr - rl) / dx;
     return F;
   }
 
   // rho[c] plus its interior-face terms in the reference's order:
   // new[c] += scale F(left face), then new[c] -= scale F(right face)
   __device__ __forceinline__ double base(int64_t c) const {
-    const int64_t e = d.cell_edge[c];
-    const int64_t lo = d.offs[e], hi = d.offs[e + 1];
-    const double scale = dt / d.dx_edge[e];
-    double v = rho[c];
-    if (c > lo) v += scale * face(e, lo, c);
-    if (c + 1 < hi) v -= scale * face(e, lo, c + 1);
+    const uint8_t fl = d.cell_flags[c];
+    const double D = d.cell_D[c], dx = d.cell_dx[c];
+    const double rc = rho[c];
+    const double rl = (fl & kLeft) ? rho[c - 1] : 0.0;
+    const double rr = (fl & kRight) ? rho[c + 1] : 0.0;
+    const double scale = dt / dx;
+    double v = rc;
+    if (fl & kLeft) v += scale * face(d.cell_mu_l[c], D, dx, rl, rc);
+    if (fl & kRight) v -= scale * face(d.cell_mu_r[c], D, dx, rc, rr);
     return v;
   }
 
-  // vertex exchange at v (fvm.py:305-328) applied to out[] (cells owned here),
-  // through accessors so the same loop runs on registers/local memory (small
-  // degree) or directly on global memory (hubs, shared cells)
+  // vertex exchange (fvm.py:305-328) through accessors, so the same loop runs
+  // on local arrays (small degree) or on global memory (hubs, shared cells)
   template <class Nw, class Rho, class B, class Dx, class Sp, class Dv>
   __device__ __forceinline__ void exchange(int n, Nw &&nw, Rho &&r, B &&b, Dx &&dx, Sp &&sp,
                                            Dv &&Dd) const {
@@ -98,12 +102,8 @@ struct Fvm {
     }
   }
 
-  // whole update of a vertex whose cells no other vertex touches: face terms
-  // then exchange, slot values staged in local arrays (L1) for degree <= 8
-  __device__ void vertex_private(int64_t v, double &amax, double &nmin) const;
-
-  // exchange on global memory, in place on out[] (cells already initialised)
-  __device__ void vertex(int64_t v) const {
+  // exchange in place on out[] (cells already initialised)
+  __device__ void vertex_global(int64_t v) const {
     const int64_t lo = d.v_off[v], hi = d.v_off[v + 1];
     if (hi - lo < 2) return;
     const int64_t *cell = d.v_cells + lo;
@@ -123,108 +123,138 @@ __device__ __forceinline__ void track(double v, double &amax, double &nmin) {
   nmin = fmax(nmin, -v);
 }
 
-constexpr int kLocalDeg = 8;
-
-__device__ void Fvm::vertex_private(int64_t v, double &amax, double &nmin) const {
-  const int64_t lo = d.v_off[v], hi = d.v_off[v + 1];
-  const int n = (int)(hi - lo);
-  if (n > kLocalDeg) {
-    init_cells(v);
-    vertex(v);
-    for (int64_t i = lo; i < hi; ++i) track(out[d.v_cells[i]], amax, nmin);
-    return;
+// New density of the cell of slot k of vertex v (cells of v touched by no
+// other vertex): its face terms, then exactly the contributions the
+// reference's exchange loop (fvm.py:305-328) adds to THIS cell, in loop order.
+// Terms are recomputed per slot (the same IEEE operations as the serial loop),
+// so one vertex's slots update in parallel: O(deg) per thread, not O(deg^2).
+__device__ double slot_update(const Fvm &f, int64_t v, int k) {
+  const gsde_fvm_desc &d = f.d;
+  const int64_t lo = d.v_off[v];
+  const int n = (int)(d.v_off[v + 1] - lo);
+  const double *b = d.v_b + lo, *dx = d.v_dx + lo, *sp = d.v_speed_in + lo, *Dd = d.v_D + lo;
+  const int64_t *cell = d.v_cells + lo;
+  const double dt = f.dt;
+  double acc = f.base(cell[k]);
+  const double bk = b[k], dxk = dx[k], rk = f.rho[cell[k]];
+  for (int i = 0; i < n; ++i) {
+    const double bi = b[i];
+    const double rho_i = i == k ? rk : f.rho[cell[i]];
+    if (sp[i] > 0.0) {
+      const double others = 1.0 - bi;
+      if (others > 0.0) {
+        const double total = sp[i] * rho_i;
+        if (i == k) {  // cell i exports to every other slot, in j order
+          for (int j = 0; j < n; ++j) {
+            if (j == i) continue;
+            const double fl = total * b[j] / others;
+            acc -= dt * fl / dxk;
+          }
+        } else {  // cell k receives its share once
+          const double fl = total * bk / others;
+          acc += dt * fl / dxk;
+        }
+      }
+    }
+    if (i > k) continue;  // pairs (i, j > i) touching k need i <= k
+    const double conc_i = rho_i / bi;
+    for (int j = (i == k ? i + 1 : k); j < (i == k ? n : k + 1); ++j) {
+      const double dpair = 0.5 * (Dd[i] + Dd[j]);
+      const double dxh = 2.0 * dx[i] * dx[j] / (dx[i] + dx[j]);
+      const double rj = j == k ? rk : f.rho[cell[j]];
+      const double g = dpair * (conc_i - rj / b[j]) / dxh;
+      if (g >= 0.0) {
+        const double fl = g * b[j];
+        if (j == k)
+          acc += dt * fl / dx[j];
+        else
+          acc -= dt * fl / dx[i];
+      } else {
+        const double fl = -g * b[i];
+        if (i == k)
+          acc += dt * fl / dx[i];
+        else
+          acc -= dt * fl / dx[j];
+      }
+    }
   }
-  double nw[kLocalDeg], r[kLocalDeg], b[kLocalDeg], dx[kLocalDeg], sp[kLocalDeg], Dd[kLocalDeg];
-  int64_t cell[kLocalDeg];
-  for (int k = 0; k < n; ++k) {
-    cell[k] = d.v_cells[lo + k];
-    nw[k] = base(cell[k]);
-    r[k] = rho[cell[k]];
-    b[k] = d.v_b[lo + k];
-    dx[k] = d.v_dx[lo + k];
-    sp[k] = d.v_speed_in[lo + k];
-    Dd[k] = d.v_D[lo + k];
-  }
-  exchange(n, [&](int k) -> double & { return nw[k]; }, [&](int k) { return r[k]; },
-           [&](int k) { return b[k]; }, [&](int k) { return dx[k]; },
-           [&](int k) { return sp[k]; }, [&](int k) { return Dd[k]; });
-  for (int k = 0; k < n; ++k) {
-    out[cell[k]] = nw[k];
-    track(nw[k], amax, nmin);
-  }
+  return acc;
 }
 
 __global__ void __launch_bounds__(kFvmThreads)
-    fvm_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch, int64_t n_steps, double dt,
-               double neg_floor, int64_t *neg_step, unsigned long long *red) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double s_amax[kFvmThreads / 32], s_nmin[kFvmThreads / 32];
-  const int64_t n_items = d.n_cells + d.n_vpar + (d.n_vser > 0 ? 1 : 0);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool leader = tid == 0;
-  if (leader) *neg_step = 0;
-  int64_t done = 0;
-  for (int64_t step = 0; step < n_steps; ++step) {
-    Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
-    double amax = 0.0, nmin = 0.0;  // max |rho|, max(-rho) over the cells written here
-    for (int64_t it = tid; it < n_items; it += stride) {
-      if (it < d.n_cells) {
-        if (d.owned[it]) continue;
-        const double v = f.base(it);
-        f.out[it] = v;
-        track(v, amax, nmin);
-      } else if (it < d.n_cells + d.n_vpar) {
-        f.vertex_private(d.vpar[it - d.n_cells], amax, nmin);
-      } else {
-        for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
-        for (int64_t k = 0; k < d.n_vser; ++k) f.vertex(d.vser[k]);
-        for (int64_t k = 0; k < d.n_vser; ++k)
-          for (int64_t i = d.v_off[d.vser[k]]; i < d.v_off[d.vser[k] + 1]; ++i)
-            track(f.out[d.v_cells[i]], amax, nmin);
-      }
+    fvm_step_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
+                    double dt, double neg_floor, int64_t *neg_step,
+                    unsigned long long *red) {
+  if (*(volatile int64_t *)neg_step) return;  // an earlier step went negative
+  const int64_t step = (int64_t)red[3];
+  const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double amax = 0.0, nmin = 0.0;  // max |rho|, max(-rho) over the cells written here
+  if (it < d.n_cells) {
+    if (!(d.cell_flags[it] & kOwned)) {
+      const double v = f.base(it);
+      f.out[it] = v;
+      track(v, amax, nmin);
     }
-    // block max, then one atomic per block into this step's slot (ring of 3:
-    // the slot reset here was last read before the previous barrier)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      nmin = fmax(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      s_amax[threadIdx.x >> 5] = amax;
-      s_nmin[threadIdx.x >> 5] = nmin;
-    }
-    __syncthreads();
-    unsigned long long *slot = red + 2 * (step % 3);
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < kFvmThreads / 32; ++w) {
-        amax = fmax(amax, s_amax[w]);
-        nmin = fmax(nmin, s_nmin[w]);
-      }
-      // canonical +0: the bit-pattern max below orders non-negative doubles only
-      amax = amax > 0.0 ? amax : 0.0;
-      nmin = nmin > 0.0 ? nmin : 0.0;
-      atomicMax(&slot[0], (unsigned long long)__double_as_longlong(amax));
-      atomicMax(&slot[1], (unsigned long long)__double_as_longlong(nmin));
-      if (leader) {
-        unsigned long long *next = red + 2 * ((step + 1) % 3);
-        next[0] = 0ull;
-        next[1] = 0ull;
-      }
-    }
-    grid.sync();
-    done = step + 1;
-    const double mx = fmax(1.0, __longlong_as_double((long long)*(volatile unsigned long long *)&slot[0]));
-    const double mn = -__longlong_as_double((long long)*(volatile unsigned long long *)&slot[1]);
-    if (mn < neg_floor * mx) {
-      if (leader) *neg_step = step + 1;
-      break;
-    }
+  } else if (it < d.n_cells + d.n_pslot) {
+    const int64_t sl = d.pslot[it - d.n_cells];
+    const int64_t v = d.slot_vertex[sl];
+    const double val = slot_update(f, v, (int)(sl - d.v_off[v]));
+    f.out[d.v_cells[sl]] = val;
+    track(val, amax, nmin);
+  } else if (it == d.n_cells + d.n_pslot && d.n_vser > 0) {
+    for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
+    for (int64_t k = 0; k < d.n_vser; ++k) f.vertex_global(d.vser[k]);
+    for (int64_t k = 0; k < d.n_vser; ++k)
+      for (int64_t i = d.v_off[d.vser[k]]; i < d.v_off[d.vser[k] + 1]; ++i)
+        track(f.out[d.v_cells[i]], amax, nmin);
   }
-  // after an odd number of steps the newest density is in scratch: move it
-  if (done & 1)
-    for (int64_t c = tid; c < d.n_cells; c += stride) rho[c] = scratch[c];
+  __shared__ double s_amax[kFvmThreads / 32], s_nmin[kFvmThreads / 32];
+  __shared__ bool s_last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    nmin = fmax(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_amax[threadIdx.x >> 5] = amax;
+    s_nmin[threadIdx.x >> 5] = nmin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kFvmThreads / 32; ++w) {
+      amax = fmax(amax, s_amax[w]);
+      nmin = fmax(nmin, s_nmin[w]);
+    }
+    // canonical +0: the bit-pattern max below orders non-negative doubles only
+    amax = amax > 0.0 ? amax : 0.0;
+    nmin = nmin > 0.0 ? nmin : 0.0;
+    atomicMax(&red[0], (unsigned long long)__double_as_longlong(amax));
+    atomicMax(&red[1], (unsigned long long)__double_as_longlong(nmin));
+    __threadfence();
+    s_last = atomicAdd(&red[2], 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {  // every block's maxima are in: the stop test
+    __threadfence();
+    const volatile unsigned long long *vr = red;
+    const double mx = fmax(1.0, __longlong_as_double((long long)vr[0]));
+    const double mn = -__longlong_as_double((long long)vr[1]);
+    if (mn < neg_floor * mx) *neg_step = step + 1;
+    red[0] = 0ull;
+    red[1] = 0ull;
+    red[2] = 0ull;
+    red[3] = (unsigned long long)(step + 1);
+  }
+}
+
+// after an odd number of completed steps the newest density is in scratch
+__global__ void fvm_finish_kernel(double *rho, const double *scratch, int64_t n_cells,
+                                  const unsigned long long *red) {
+  if (!(red[3] & 1ull)) return;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
+       c += (int64_t)gridDim.x * blockDim.x)
+    rho[c] = scratch[c];
 }
 
 }  // namespace
@@ -232,25 +262,26 @@ __global__ void __launch_bounds__(kFvmThreads)
 cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int64_t n_steps,
                        double dt, double neg_floor, int64_t *neg_step, uint64_t *red,
                        cudaStream_t s) {
-  int device = 0;
-  cudaError_t err = cudaGetDevice(&device);
-  if (err != cudaSuccess) return err;
-  int per_sm = 0;
-  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fvm_kernel, kFvmThreads, 0);
-  if (err != cudaSuccess) return err;
-  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-  const int64_t items = d.n_cells + d.n_vpar + 1;
-  int64_t grid = (int64_t)dev_info(device).sm_count * per_sm;
-  const int64_t need = (items + kFvmThreads - 1) / kFvmThreads;
-  if (need < grid) grid = need < 1 ? 1 : need;
-  err = cudaMemsetAsync(red, 0, 6 * sizeof(uint64_t), s);
+  cudaError_t err = cudaMemsetAsync(red, 0, 4 * sizeof(uint64_t), s);
+  if (err == cudaSuccess) err = cudaMemsetAsync(neg_step, 0, sizeof(int64_t), s);
   if (err != cudaSuccess) return err;
   unsigned long long *r = reinterpret_cast<unsigned long long *>(red);
-  void *args[] = {(void *)&d, &rho, &scratch, &n_steps, &dt, &neg_floor, &neg_step, &r};
-  err = cudaLaunchCooperativeKernel((const void *)fvm_kernel, dim3((unsigned)grid),
-                                    dim3(kFvmThreads), args, 0, s);
+  const int64_t items = d.n_cells + d.n_pslot + (d.n_vser > 0 ? 1 : 0);
+  const unsigned grid = (unsigned)((items + kFvmThreads - 1) / kFvmThreads);
+  for (int64_t k = 0; k < n_steps; ++k) {
+    fvm_step_kernel<<<grid, kFvmThreads, 0, s>>>(d, rho, scratch, dt, neg_floor, neg_step, r);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  count_launch((int)(n_steps < (1 << 30) ? n_steps : (1 << 30)));
+  int device = 0;
+  cudaGetDevice(&device);
+  const int64_t blocks = (d.n_cells + kFvmThreads - 1) / kFvmThreads;
+  const int64_t cap = (int64_t)dev_info(device).sm_count * 8;
+  fvm_finish_kernel<<<(unsigned)(blocks < cap ? blocks : cap), kFvmThreads, 0, s>>>(
+      rho, scratch, d.n_cells, r);
   count_launch();
-  return err;
+  return cudaGetLastError();
 }
 
 }  // namespace gsde

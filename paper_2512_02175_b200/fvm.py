@@ -190,6 +190,15 @@ class _Packed:
     owned: np.ndarray
     vpar: np.ndarray
     vser: np.ndarray
+    slot_vertex: np.ndarray
+    pslot: np.ndarray
+    # per-cell records of the GPU stepper: drift on the left / right interior
+    # face, D and dx of the cell's edge, flags (1 left face, 2 right face, 4 owned)
+    cell_mu_l: np.ndarray
+    cell_mu_r: np.ndarray
+    cell_D: np.ndarray
+    cell_dx: np.ndarray
+    cell_flags: np.ndarray
 
     def reference_tuple(self):
         return (self.offs, self.dx_edge, self.D_edge, self.face_mu, self.face_off, self.v_off,
@@ -233,13 +242,29 @@ def _pack(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> _Packe
     shared = np.zeros(deg.shape[0], dtype=bool)
     shared[np.unique(slot_vertex[multi & (owners[v_cells] >= 2)])] = True
     hub = deg >= 2
+    cell_edge = np.repeat(np.arange(E, dtype=np.int64), counts)
+    local = np.arange(n_cells, dtype=np.int64) - offs[cell_edge]
+    left = local > 0
+    right = local + 1 < counts[cell_edge]
+    # face k of edge e (between its cells k and k+1) sits at face_mu[face_off[e] + k]
+    fidx = face_off[cell_edge] + local
+    cell_mu_l = np.zeros(n_cells)
+    cell_mu_r = np.zeros(n_cells)
+    cell_mu_l[left] = face_mu[fidx[left] - 1]
+    cell_mu_r[right] = face_mu[fidx[right]]
+    owned = owners >= 1
+    flags = (left.astype(np.uint8) | (right.astype(np.uint8) << 1)
+             | (owned.astype(np.uint8) << 2))
     return _Packed(
         offs=offs, dx_edge=dx, D_edge=D_edge, face_mu=face_mu, face_off=face_off, v_off=v_off,
         v_cells=v_cells, v_b=v_b, v_dx=v_dx, v_speed_in=v_speed_in, v_D=v_D,
-        cell_edge=np.repeat(np.arange(E, dtype=np.int64), counts),
-        owned=(owners >= 1).astype(np.uint8),
+        cell_edge=cell_edge, owned=owned.astype(np.uint8),
         vpar=np.flatnonzero(hub & ~shared).astype(np.int64),
-        vser=np.flatnonzero(hub & shared).astype(np.int64))
+        vser=np.flatnonzero(hub & shared).astype(np.int64),
+        slot_vertex=slot_vertex,
+        pslot=np.flatnonzero((hub & ~shared)[slot_vertex]).astype(np.int64),
+        cell_mu_l=cell_mu_l, cell_mu_r=cell_mu_r, cell_D=D_edge[cell_edge].copy(),
+        cell_dx=dx[cell_edge].copy(), cell_flags=flags.astype(np.uint8))
 
 
 def stability_limit(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> float:
@@ -276,11 +301,15 @@ def stability_limit(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid)
     return 1.0 / max_rate
 
 
+_DESC_ARRAYS = ("cell_mu_l", "cell_mu_r", "cell_D", "cell_dx", "cell_flags", "v_off", "v_cells",
+                "v_b", "v_dx", "v_speed_in", "v_D", "slot_vertex", "pslot", "vser")
+
+
 class _Desc(C.Structure):
-    _fields_ = [(n, C.c_int64) for n in ("n_edges", "n_cells", "n_vertices", "n_vpar", "n_vser")] + [
-        (n, C.c_void_p) for n in ("offs", "dx_edge", "D_edge", "face_mu", "face_off", "v_off",
-                                  "v_cells", "v_b", "v_dx", "v_speed_in", "v_D", "cell_edge",
-                                  "owned", "vpar", "vser")]
+    """``gsde_fvm_desc`` (include/gsde.h)."""
+
+    _fields_ = [(n, C.c_int64) for n in ("n_edges", "n_cells", "n_vertices", "n_pslot", "n_vser")] + [
+        (n, C.c_void_p) for n in _DESC_ARRAYS]
 
 
 def _device_pack(p: _Packed, n_vertices: int, device: int):
@@ -289,9 +318,8 @@ def _device_pack(p: _Packed, n_vertices: int, device: int):
     keep = {}
     d = _Desc()
     d.n_edges, d.n_cells = p.dx_edge.shape[0], p.cell_edge.shape[0]
-    d.n_vertices, d.n_vpar, d.n_vser = n_vertices, p.vpar.shape[0], p.vser.shape[0]
-    for name in ("offs", "dx_edge", "D_edge", "face_mu", "face_off", "v_off", "v_cells", "v_b",
-                 "v_dx", "v_speed_in", "v_D", "cell_edge", "owned", "vpar", "vser"):
+    d.n_vertices, d.n_pslot, d.n_vser = n_vertices, p.pslot.shape[0], p.vser.shape[0]
+    for name in _DESC_ARRAYS:
         a = getattr(p, name)
         t = torch.from_numpy(np.ascontiguousarray(a) if a.size else np.zeros(1, a.dtype)).to(**kw)
         keep[name] = t
