@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
 // fused exit counts per edge and M histogram including M = 0.
-template <class C>
+template <class C, bool OUT>
 __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv) {
   const int nb = p.cap + 1;
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   Lane<C> L;
   uint32_t pair = 0;
   uint64_t id = 0;
-  int64_t t_M = 0, t_ev = 0, t_tr = 0;
+  int32_t t_M = 0, t_ev = 0, t_tr = 0;  // per lane: <= ~1e4 trials x cap
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
     L.load_edge(T, O, C::STAR ? 0 : p.start_edge, p.sqdt, inf);
@@ -702,10 +702,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     pair = 0;
   };
   auto finish = [&]() {
-    if (o.M) o.M[i] = L.M;
-    if (o.edge) o.edge[i] = L.e;
-    if (o.x) o.x[i] = (double)L.x;
-    if (o.trunc) o.trunc[i] = L.trunc ? 1 : 0;
+    if (OUT) {  // per-trial arrays (vertex_crossing_trials); the fused estimator skips them
+      if (o.M) o.M[i] = L.M;
+      if (o.edge) o.edge[i] = L.e;
+      if (o.x) o.x[i] = (double)L.x;
+      if (o.trunc) o.trunc[i] = L.trunc ? 1 : 0;
+    }
     if (S.exit_priv)
       S.exit_priv[L.e * kThreads + threadIdx.x] += 1;
     else if (o.exit_counts)
@@ -903,7 +905,9 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   const int d = g->device;
   const int64_t n = a.n_trials;
   return dispatch<false>(g->is_star, stage, g->has_tab, false, [&](auto cfg) -> cudaError_t {
-    auto k = native_trials_kernel<decltype(cfg)>;
+    const bool out = o.M || o.edge || o.x || o.trunc;
+    auto k = out ? native_trials_kernel<decltype(cfg), true>
+                 : native_trials_kernel<decltype(cfg), false>;
     cudaError_t err = prepare(k, smem);
     if (err != cudaSuccess) return err;
     return launch(k, smem, occupancy_grid(k, smem, d, n), s, g->nat, p, o, priv);
