@@ -130,7 +130,7 @@ __device__ __forceinline__ Block native_block(const NatParams &p, uint32_t pair,
   return c;
 }
 
-__device__ __forceinline__ size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
 // Graph tables: shared-memory copies (SMEM) or global/L2 (read-only path).
 template <bool SMEM>
@@ -501,12 +501,11 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
   return done;
 }
 
-template <class C>
-__device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
-                                             const Tables<C::SMEM> &T, const Occ &O,
-                                             const NatParams &p, uint64_t id, float star_len) {
-  int e;
-  float x;
+// Initial state of particle id (kernels.py:291-307, engine.py:194-203): the
+// edge and position only.
+template <bool SMEM>
+__device__ __forceinline__ void place_values(const NativeGraph &G, const Tables<SMEM> &T,
+                                             const NatParams &p, uint64_t id, int &e, float &x) {
   if (p.init_kind == GSDE_INIT_POINT) {
     e = p.init_edge;
     x = p.init_x;
@@ -519,6 +518,12 @@ __device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
     const double le = (double)T.E(e).x;
     x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
   }
+}
+
+template <class C>
+__device__ __forceinline__ void start_particle(Lane<C> &L, const Tables<C::SMEM> &T,
+                                               const Occ &O, const NatParams &p, int e, float x,
+                                               float star_len) {
   L.load_edge(T, O, e, p.sqdt, star_len);
   L.x = x;
   L.dtr = p.dt;
@@ -530,6 +535,33 @@ __device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
   L.cross = L.events = L.truncs = 0;
   L.occ_left = O.start + O.every;
 }
+
+template <class C>
+__device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
+                                             const Tables<C::SMEM> &T, const Occ &O,
+                                             const NatParams &p, uint64_t id, float star_len) {
+  int e;
+  float x;
+  place_values<C::SMEM>(G, T, p, id, e, x);
+  start_particle<C>(L, T, O, p, e, x, star_len);
+}
+
+// Per-warp shared queues of the ensemble kernel (64-entry rings):
+//  * placements: particle index, edge and position of the next particles,
+//    filled 32 at a time in one converged pass (one atomic, 32 Philox blocks
+//    and 32 edge-record loads in flight together);
+//  * finished states: edge and position awaiting the fused estimators,
+//    binned 32 at a time in one converged pass (the dependent grid loads of
+//    32 particles in flight together).
+constexpr int kRing = 64;
+struct WarpQueues {
+  long long *pid;
+  int *pe;
+  float *px;
+  int *fe;
+  float *fx;
+};
+constexpr size_t kQueueBytesPerWarp = kRing * (sizeof(long long) + 2 * sizeof(int) + 2 * sizeof(float));
 
 // Random words of one Q-trip iteration with SLOTS vertex slots (trips
 // k Q / SLOTS): word 0 = slot 0's exit uniform, words 1..Q = Box-Muller
@@ -561,7 +593,7 @@ struct IterWords {
 template <class C, int Q, int SLOTS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
-                           unsigned long long *work) {
+                           unsigned long long *work, unsigned queue_off) {
   using IW = IterWords<Q, SLOTS>;
   constexpr int NB = IW::NB;
   const int nb = p.cap + 1;
@@ -587,12 +619,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   bool waiting = i < p.n;  // next particle not started yet
   bool active = false;     // a particle is in flight
   bool need = false;       // finished: fetch the next particle id
+  bool queued = false;     // this lane's finished state awaits binning
 
   auto finish = [&]() {
     t_cross += L.cross;
     t_events += L.events;
     t_truncs += L.truncs;
-    ensemble_epilogue(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
+    epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
+    queued = true;
     active = false;
     need = true;
   };
@@ -600,42 +634,93 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     while (waiting) {
       id = (uint64_t)(p.id_offset + i);
       place_native(L, G, T, O, p, id, star_len);
-      finish();
+      epilogue_particle(o, i, L.e, (double)L.x, 0, 0, 0);
+      epilogue_bins(o, L.e, (double)L.x);
       i += stride;
       waiting = i < p.n;
     }
-    need = false;
     L.steps_left = 0;
   }
 
-  // First particle: the thread index; then dynamic, from a grid-wide counter
-  // with one warp-aggregated atomic per batch of finishing lanes, so warps
-  // the schedulers favour take more particles and the SMs stay full until the
-  // end (results are per particle id and integer sums: assignment-invariant).
+  // Particles come from a grid-wide counter, 32 per warp refill, so warps the
+  // schedulers favour take more particles and the SMs stay full until the end
+  // (results are per particle id and integer sums: assignment-invariant).
   // Particles start on iteration boundaries, so the lanes of a warp share
   // their vertex slot.
   const int lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) unsigned char smem_q[];
+  WarpQueues WQ;
+  {
+    unsigned char *q = smem_q + queue_off + (threadIdx.x >> 5) * kQueueBytesPerWarp;
+    WQ.pid = reinterpret_cast<long long *>(q);
+    WQ.pe = reinterpret_cast<int *>(q + kRing * sizeof(long long));
+    WQ.px = reinterpret_cast<float *>(q + kRing * (sizeof(long long) + sizeof(int)));
+    WQ.fe = reinterpret_cast<int *>(q + kRing * (sizeof(long long) + sizeof(int) + sizeof(float)));
+    WQ.fx = reinterpret_cast<float *>(q + kRing * (sizeof(long long) + 2 * sizeof(int) + sizeof(float)));
+  }
+  uint32_t q_head = 0, q_tail = 0;  // placement ring (warp-uniform)
+  int f_n = 0;                      // finished states queued (warp-uniform)
+  const bool bins = o.edge_counts || o.hist;
+  auto flush_bins = [&](int n_take) {  // converged: bin entries 0..n_take-1
+    if (lane < n_take) epilogue_bins(o, WQ.fe[lane], (double)WQ.fx[lane]);
+    __syncwarp();
+    if (lane < f_n - n_take) {  // n_take == 32: sources and targets do not overlap
+      WQ.fe[lane] = WQ.fe[n_take + lane];
+      WQ.fx[lane] = WQ.fx[n_take + lane];
+    }
+    __syncwarp();
+    f_n -= n_take;
+  };
+  need = true;
+  waiting = false;
   for (;;) {
-    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    const unsigned nm = __ballot_sync(0xffffffffu, need);  // finished lanes (+ the start)
     if (nm) {
-      const int leader = __ffs(nm) - 1;
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(work, (unsigned long long)__popc(nm));
-      base = __shfl_sync(0xffffffffu, base, leader);
+      if (bins) {  // queue the finished states; bin 32 at a time
+        const unsigned qm = __ballot_sync(0xffffffffu, queued);
+        if (queued) {
+          const int slot = f_n + __popc(qm & ((1u << lane) - 1u));
+          WQ.fe[slot] = L.e;
+          WQ.fx[slot] = L.x;
+          queued = false;
+        }
+        f_n += __popc(qm);
+        __syncwarp();
+        if (f_n >= 32) flush_bins(32);
+      }
+      const int k = __popc(nm);
+      if (q_tail - q_head < (uint32_t)k) {  // refill 32 placements
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(work, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int64_t pi = (int64_t)base + lane;
+        int e = 0;
+        float x = 0.0f;
+        if (pi < p.n) place_values<C::SMEM>(G, T, p, (uint64_t)(p.id_offset + pi), e, x);
+        const int slot = (int)((q_tail + lane) & (kRing - 1));
+        WQ.pid[slot] = pi;
+        WQ.pe[slot] = e;
+        WQ.px[slot] = x;
+        q_tail += 32;
+        __syncwarp();
+      }
       if (need) {
-        i = stride + (int64_t)base + __popc(nm & ((1u << lane) - 1u));
+        const int slot = (int)((q_head + __popc(nm & ((1u << lane) - 1u))) & (kRing - 1));
+        i = WQ.pid[slot];
         waiting = i < p.n;
+        if (waiting) {
+          id = (uint64_t)(p.id_offset + i);
+          start_particle<C>(L, T, O, p, WQ.pe[slot], WQ.px[slot], star_len);
+          blk = 0;
+          waiting = false;
+          active = true;
+        }
         need = false;
       }
+      q_head += k;
+      __syncwarp();
     }
-    if (!__any_sync(0xffffffffu, active || waiting)) break;
-    if (waiting) {
-      id = (uint64_t)(p.id_offset + i);
-      place_native(L, G, T, O, p, id, star_len);
-      blk = 0;
-      waiting = false;
-      active = true;
-    }
+    if (!__any_sync(0xffffffffu, active)) break;
     uint32_t W[4 * NB];
     auto fill = [&](int kb) {
       const Block r = native_block(p, blk + (uint32_t)kb, kDomainEnsemble, id);
@@ -664,6 +749,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     blk += NB;
     if (active && L.steps_left == 0) finish();
   }
+  if (bins && f_n > 0) flush_bins(f_n);
   if (o.totals) {
     warp_add_i64(&o.totals[0], t_cross);
     warp_add_i64(&o.totals[1], t_events);
@@ -872,7 +958,8 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     // per-block count can overflow 32 bits
     int occ_cells = 0;
     if (C::OCC && o.hist_n_cells <= kOccSmemCells) occ_cells = (int)o.hist_n_cells;
-    size_t smem = smem_bytes(g, a.cap + 1, stage, false, occ_cells);
+    const size_t queues = (kThreads / 32) * kQueueBytesPerWarp;
+    size_t smem = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells)) + queues;
     cudaError_t err = prepare(k, smem);
     if (err != cudaSuccess) return err;
     const int grid = occupancy_grid(k, smem, d, n);
@@ -881,14 +968,15 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
                                ((double)a.n_steps / (double)(o.occ_every > 0 ? o.occ_every : 1));
       if (per_block >= 4.0e9) occ_cells = 0;
     }
-    smem = smem_bytes(g, a.cap + 1, stage, false, occ_cells);
+    const size_t qoff = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells));
+    smem = qoff + queues;
     // grid-wide particle counter: this call's slot of the handle's ring
     // (a per-call cudaMallocAsync here stalled running kernels for up to
     // hundreds of ms when the pool remapped memory)
     unsigned long long *work = const_cast<gsde_graph *>(g)->next_work_slot();
     err = cudaMemsetAsync(work, 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
-    return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work);
+    return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff);
   };
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run)
              : dispatch<false>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run);
