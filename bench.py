@@ -517,6 +517,11 @@ def main():
 
     import torch
 
+    # GSDE_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0, gloo collectives --
+    # exercises the multi-rank sharding / reduction / max-over-ranks logic on a 1-GPU box
+    shared = os.environ.get("GSDE_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = local
     dist = None
@@ -524,7 +529,10 @@ def main():
         import torch.distributed as tdist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         dist = tdist
     import paper_2512_02175_b200 as gs  # noqa: F401
     from paper_2512_02175_b200 import _native
