@@ -575,7 +575,8 @@ def main():
                    "d2h_bytes_per_step": int(nbytes),
                    "ms_per_call": [round(t * 1e3, 2) for t in times],
                    "path": "paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble): graph "
-                           "upload, kernel, pinned D2H of the reference-dtype result arrays"}
+                           "upload, kernel, pinned D2H of the reference-dtype result arrays "
+                           "(4 particle-id chunks: each chunk's D2H overlaps the next kernel)"}
         line = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,

@@ -288,9 +288,8 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
         z = np.zeros(0, np.int64)
         stats = BounceStats(np.zeros(cap + 1, np.int64), run_gamma, 0, 0, 0)
         return EnsembleResult(z, np.zeros(0), z.copy(), z.copy(), stats, config)
-    res = ensemble_device(graph, field, config, outputs=("edge", "x", "crossings", "events"))
-    edges, positions, crossings, events, m_hist, totals = _to_host(
-        [res[k] for k in ("edge", "x", "crossings", "events", "m_hist", "totals")])
+    edges, positions, crossings, events, m_hist, totals = _ensemble_to_host(graph, field,
+                                                                           config)
     stats = BounceStats(
         m_histogram=m_hist,
         gamma=run_gamma,
@@ -299,6 +298,51 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
         crossing_events=int(totals[1]),
     )
     return EnsembleResult(edges, positions, crossings, events, stats, config)
+
+
+#: Particle-count split of a large run_ensemble call: chunk k's device->host
+#: copy of the per-particle arrays overlaps chunk k+1's kernel; the last chunk
+#: is the smallest, so little transfer is left exposed.
+_CHUNKS = (0.4, 0.3, 0.2, 0.1)
+_PIPELINE_MIN = 1 << 22
+
+
+def _ensemble_to_host(graph, field, config):
+    """run_ensemble's device work + transfers: per-particle arrays land in
+    pinned host memory; large runs are split by global particle id (results
+    are identical: every particle's stream is keyed by its id, the fused
+    counts are integer sums) so transfers overlap the next chunk's kernel."""
+    import torch
+
+    names = ("edge", "x", "crossings", "events")
+    n = config.n_particles
+    if n < _PIPELINE_MIN:
+        res = ensemble_device(graph, field, config, outputs=names)
+        return _to_host([res[k] for k in names + ("m_hist", "totals")])
+    _, dev = _native.torch_cuda(config.device)
+    compute = torch.cuda.current_stream(dev)
+    copier = torch.cuda.Stream(dev)
+    hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
+             for k in names]
+    bounds = np.concatenate([[0], np.cumsum(np.floor(np.array(_CHUNKS) * n).astype(np.int64))])
+    bounds[-1] = n
+    parts = []
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        if hi <= lo:
+            continue
+        res = ensemble_device(graph, field, config, pid_offset=int(lo), n_particles=int(hi - lo),
+                              outputs=names, stream=compute.cuda_stream)
+        done = torch.cuda.Event()
+        done.record(compute)
+        copier.wait_event(done)
+        with torch.cuda.stream(copier):
+            for h, k in zip(hosts, names):
+                h[lo:hi].copy_(res[k], non_blocking=True)
+        parts.append(res)  # keeps the device buffers alive until the copies finished
+    copier.synchronize()
+    m_hist = sum(r["m_hist"] for r in parts).cpu().numpy()
+    totals = sum(r["totals"] for r in parts).cpu().numpy()
+    return [h.numpy() for h in hosts] + [m_hist, totals]
 
 
 def _bits64(v: int) -> int:
