@@ -229,6 +229,14 @@ def make_workload(name, rank, world):
             _vascular_cached, 100_000_000, 100, 1e-3,
             lambda g: gs.PerEdgeUniform(float(g.edge_length.max())),
             lambda g: gs.EdgeGrid.uniform(g, 8), rank, world)
+    if name == "vascular_c5":  # C5: 1e8 particles x 100 steps in TOTAL, sharded over the ranks
+        return Ensemble(
+            "vascular_c5", "C5: the C4 network, 1e10 particle-steps per bench step in total "
+            "(1e8 particles x 100 steps) sharded by particle id across the GPUs; per-step NCCL "
+            "all-reduce of the fused estimators (8-cell/edge histogram, edge counts, M histogram)",
+            _vascular_cached, 100_000_000 // world, 100, 1e-3,
+            lambda g: gs.PerEdgeUniform(float(g.edge_length.max())),
+            lambda g: gs.EdgeGrid.uniform(g, 8), rank, world)
     if name == "star5_trials":
         return Trials(rank, world)
     if name == "fvm":
@@ -627,6 +635,19 @@ def main():
                                 "step_ms": list(STEP_MS), "crossings_per_unit": c2,
                                 "roofline_frac": rate2 * lane_ops_per_pstep(c2) / peak_ops}
             line["workloads"] = extras
+    if not args.no_extras:
+        # C5 strong scaling on every rank (a collective run): fixed 1e10 psteps per step
+        w5 = make_workload("vascular_c5", rank, world)
+        t5, _, r5, _, _ = time_workload(w5, 3, 2, dist, torch, dev, flush_buf)
+        if rank == 0:
+            rate5 = w5.units_per_step * world * 3 / t5
+            c5 = w5.crossings(r5) / w5.units_per_step
+            line.setdefault("workloads", {})["vascular_c5"] = {
+                "value": rate5, "unit": w5.unit, "scaling": "strong", "n_gpus": world,
+                "config": dict(w5.config(), parallelism=f"particle-sharded x{world}"),
+                "step_ms": list(STEP_MS), "crossings_per_unit": c5,
+                "roofline_frac": rate5 / world * lane_ops_per_pstep(c5) / peak_ops}
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
