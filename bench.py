@@ -154,6 +154,16 @@ class Trials(Workload):
     def crossings(self, res):
         return int(res["totals"].view(-1, 4)[:, 0].sum())
 
+    def cpu_run(self, n, threads):
+        """The same dt sweep on the CPU port: n trials split evenly over the dts."""
+        from oracle import oracle
+
+        og = oracle.OracleGraph(self.g, self.f)
+        per = max(1, n // len(self.dts))
+        for i, dt in enumerate(self.dts):
+            oracle.vertex_trials(og, 11 + i, per, dt, threads=threads)
+        return per * len(self.dts)
+
 
 class FvmWork(Workload):
     """Finite-volume baseline on the C4 network: 8 cells per edge,
@@ -379,14 +389,11 @@ def cpu_baseline(wl, seconds=12.0):
 
     threads = os.cpu_count() or 1
     if isinstance(wl, Trials):
-        og = oracle.OracleGraph(wl.g, wl.f)
-        n_cal = 200_000
         t0 = time.perf_counter()
-        oracle.vertex_trials(og, 11, n_cal, wl.dt, threads=threads)
+        n_cal = wl.cpu_run(200_000, threads)
         rate = n_cal / max(time.perf_counter() - t0, 1e-6)
-        n = int(min(max(rate * seconds, n_cal), 2e9))
         t0 = time.perf_counter()
-        oracle.vertex_trials(og, 11, n, wl.dt, threads=threads)
+        n = wl.cpu_run(int(min(max(rate * seconds, n_cal), 2e9)), threads)
         dt = time.perf_counter() - t0
         return {"value": n / dt, "unit": wl.unit, "cores": threads, "kind": "port",
                 "sample": f"{n} trials (oracle/gsde_oracle.c, {threads} threads)",
@@ -414,10 +421,10 @@ def run_reference_arm(args, rank, world):
 
     threads = os.cpu_count() or 1
     if isinstance(wl, Trials):
-        og = oracle.OracleGraph(wl.g, wl.f)
-        n = int(rate * 2.0)
-        step = lambda: oracle.vertex_trials(og, 11, n, wl.dt, threads=threads)
-        units, sample = n, f"{n} trials per step"
+        n = max(len(wl.dts), int(rate * 2.0))
+        units = max(1, n // len(wl.dts)) * len(wl.dts)
+        step = lambda: wl.cpu_run(n, threads)
+        sample = f"{units} trials per step over dt = {', '.join(f'{d:g}' for d in wl.dts)}"
     else:
         run, units, sample = wl.cpu_sample(max(4096, rate * 2.0 / wl.n_steps))
         step = lambda: run(threads)
