@@ -374,12 +374,14 @@ def load_traffic(workload):
 
 
 # ----------------------------------------------------------------------------
-#: Measured in the build container (8-core Xeon, AVX-512): the reference's own
-#: numba kernels run C1 at 3.64e7 psteps/s/thread (2.47e8 on 8 threads); the
-#: strict-IEEE C port runs 2.39e7 (1.63e8).  The port is the traveling stand-in
-#: (the Python reference cannot run on the GPU box), so CPU ratios computed
-#: against it overstate the speed-up vs the reference by about this factor.
-REFERENCE_OVER_PORT = 2.47e8 / 1.63e8
+#: Measured in the build container (8-core Xeon, AVX-512; C1, 4e5 particles x
+#: 1000 steps, warm JIT, 8 threads, three runs each): the reference's own numba
+#: kernels (fastmath) run 5.4e8-6.4e8 psteps/s, the strict-IEEE C port 3.2e8-3.6e8
+#: (an -O3 -march=native -ffast-math build of the port: 3.6e8-3.8e8).  The port
+#: is the traveling stand-in (the Python reference cannot run on the GPU box), so
+#: CPU ratios computed against it overstate the speed-up vs the reference by
+#: about this factor.
+REFERENCE_OVER_PORT = 5.9e8 / 3.4e8
 
 
 def cpu_baseline(wl, seconds=12.0):

@@ -146,16 +146,16 @@ typedef struct {
   uint64_t buf[ORC_BUF];
 } orc_draws;
 
-/* Refill: ORC_BUF independent Philox evaluations in a branch-free loop the
- * compiler vectorises (the reference's numba loop is vectorised the same way). */
+/* Refill: ORC_BUF/2 independent Philox blocks (each block is draws 2b and
+ * 2b+1, rng.py:45-66) in a branch-free loop the compiler vectorises; the
+ * buffer starts at an even draw index so every block is computed once. */
 __attribute__((target_clones("avx512f", "avx2", "default")))
 static void draws_refill(orc_draws *d) {
-  const uint64_t base = d->k;
+  const uint64_t base = d->k & ~(uint64_t)1;
   const uint32_t s0 = (uint32_t)d->seed, s1 = (uint32_t)(d->seed >> 32);
   const uint32_t p0 = (uint32_t)d->pid, p1 = (uint32_t)(d->pid >> 32);
-  for (int j = 0; j < ORC_BUF; ++j) {
-    const uint64_t idx = base + (uint64_t)j;
-    const uint64_t blk = idx >> 1;
+  for (int j = 0; j < ORC_BUF / 2; ++j) {
+    const uint64_t blk = (base >> 1) + (uint64_t)j;
     uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32), c2 = p0, c3 = p1;
     uint32_t k0 = s0, k1 = s1;
     for (int r = 0; r < 10; ++r) {
@@ -170,8 +170,8 @@ static void draws_refill(orc_draws *d) {
       k0 += PH_W0;
       k1 += PH_W1;
     }
-    const uint64_t even = ((uint64_t)c0 << 32) | c1, odd = ((uint64_t)c2 << 32) | c3;
-    d->buf[j] = (idx & 1u) ? odd : even;
+    d->buf[2 * j] = ((uint64_t)c0 << 32) | c1;
+    d->buf[2 * j + 1] = ((uint64_t)c2 << 32) | c3;
   }
   d->kbase = base;
 }
