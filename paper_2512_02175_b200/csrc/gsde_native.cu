@@ -182,7 +182,26 @@ struct Occ {
   int64_t *out;
   unsigned *s_cnt;   // shared counters, or null -> global atomics
   int32_t every, start;
+  const float4 *tab;  // shared per-edge {first cell, cells - 1, 1/dx, -} or null -> global
+  // grid cell of position x on edge e (floor(x/dx) clipped to the edge's cells)
+  __device__ __forceinline__ int cell(int e, float x) const {
+    int o, top;
+    float inv;
+    if (tab) {
+      const float4 r = tab[e];
+      o = __float_as_int(r.x);
+      top = __float_as_int(r.y);
+      inv = r.z;
+    } else {
+      o = (int)__ldg(off + e);
+      top = (int)__ldg(cnt + e) - 1;
+      inv = (float)(1.0 / __ldg(dx + e));
+    }
+    const int local = __float2int_rz(fminf(x * inv, (float)top));
+    return o + (local < 0 ? 0 : local);
+  }
 };
+constexpr int kOccTabEdges = 1024;  // per-edge occupation records staged in shared memory
 
 // Shared block state: lane-private M counters, M histogram, totals, staged
 // graph, occupation counters.
@@ -280,8 +299,6 @@ struct Lane {
   int steps_left;
   int cross, events, truncs;
   int occ_left;    // steps to the next occupation sample
-  int occ_off, occ_top;  // grid cells of e: first index, count - 1
-  float occ_inv;   // 1 / cell width of e
 
   __device__ __forceinline__ void load_edge(const Tables<C::SMEM> &T, const Occ &O, int e2,
                                             float sqdt, float star_len) {
@@ -297,11 +314,6 @@ struct Lane {
       len = r.x;
       ev = T.V(e2);
     }
-    if (C::OCC) {
-      occ_off = (int)O.off[e2];
-      occ_top = (int)O.cnt[e2] - 1;
-      occ_inv = (float)(1.0 / O.dx[e2]);
-    }
   }
 
   // general graphs: install already-loaded records of edge e2
@@ -314,11 +326,6 @@ struct Lane {
     sig_sqdt = r.w * sqdt;
     len = r.x;
     ev = v;
-    if (C::OCC) {
-      occ_off = (int)O.off[e2];
-      occ_top = (int)O.cnt[e2] - 1;
-      occ_inv = (float)(1.0 / O.dx[e2]);
-    }
   }
 
   __device__ __forceinline__ float drift(const NativeGraph &G, float at) const {
@@ -351,12 +358,15 @@ struct Lane {
     sq = sqdt;
   }
 
-  // occupation sample of the state after a completed step (every `every` steps)
-  __device__ __forceinline__ void occ_tick(const Occ &O) {
-    if (--occ_left == 0) {
-      occ_left = O.every;
-      const int local = __float2int_rz(fminf(x * occ_inv, (float)occ_top));
-      const int cell = occ_off + (local < 0 ? 0 : local);
+  // occupation sample of the state after a completed step (every `every`
+  // steps); predicated, so the trips of an iteration stay one straight-line
+  // block the compiler can interleave
+  __device__ __forceinline__ void occ_tick(const Occ &O, bool done) {
+    occ_left -= done ? 1 : 0;
+    const bool smp = done && occ_left == 0;
+    occ_left = smp ? O.every : occ_left;
+    const int cell = O.cell(e, x);
+    if (smp) {
       if (O.s_cnt)
         atomicAdd(&O.s_cnt[cell], 1u);
       else
@@ -496,7 +506,7 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
     done = rare_trip<C>(L, G, T, O, p, z, u);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
-  if (C::OCC && done) L.occ_tick(O);
+  if (C::OCC) L.occ_tick(O, done);
   L.steps_left -= done ? 1 : 0;
   return done;
 }
@@ -593,7 +603,8 @@ struct IterWords {
 template <class C, int Q, int SLOTS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
-                           unsigned long long *work, unsigned queue_off) {
+                           unsigned long long *work, unsigned queue_off,
+                           unsigned occ_tab_off) {
   using IW = IterWords<Q, SLOTS>;
   constexpr int NB = IW::NB;
   const int nb = p.cap + 1;
@@ -601,7 +612,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   Tables<C::SMEM> T;
   shared_setup<C::STAR, C::SMEM>(G, nb, S, T, false, C::OCC ? occ_smem_cells : 0);
   Occ O{o.hist_offsets, o.hist_counts, o.hist_dx, o.occ, S.occ, (int32_t)o.occ_every,
-        (int32_t)o.occ_start};
+        (int32_t)o.occ_start, nullptr};
+  if (C::OCC && G.n_edges <= kOccTabEdges) {
+    extern __shared__ __align__(16) unsigned char smem_t[];
+    float4 *tab = reinterpret_cast<float4 *>(smem_t + occ_tab_off);
+    for (int j = threadIdx.x; j < G.n_edges; j += blockDim.x)
+      tab[j] = make_float4(__int_as_float((int)o.hist_offsets[j]),
+                           __int_as_float((int)o.hist_counts[j] - 1),
+                           (float)(1.0 / o.hist_dx[j]), 0.0f);
+    __syncthreads();
+    O.tab = tab;
+  }
   const float star_len = C::REFLECT ? p.reflect : __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -959,7 +980,8 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     int occ_cells = 0;
     if (C::OCC && o.hist_n_cells <= kOccSmemCells) occ_cells = (int)o.hist_n_cells;
     const size_t queues = (kThreads / 32) * kQueueBytesPerWarp;
-    size_t smem = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells)) + queues;
+    const size_t occ_tab = (C::OCC && g->E <= kOccTabEdges) ? (size_t)g->E * sizeof(float4) : 0;
+    size_t smem = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells)) + queues + occ_tab;
     cudaError_t err = prepare(k, smem);
     if (err != cudaSuccess) return err;
     const int grid = occupancy_grid(k, smem, d, n);
@@ -969,14 +991,15 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
       if (per_block >= 4.0e9) occ_cells = 0;
     }
     const size_t qoff = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells));
-    smem = qoff + queues;
+    smem = qoff + queues + occ_tab;
     // grid-wide particle counter: this call's slot of the handle's ring
     // (a per-call cudaMallocAsync here stalled running kernels for up to
     // hundreds of ms when the pool remapped memory)
     unsigned long long *work = const_cast<gsde_graph *>(g)->next_work_slot();
     err = cudaMemsetAsync(work, 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
-    return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff);
+    return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
+                  (unsigned)(qoff + queues));
   };
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run)
              : dispatch<false>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run);
