@@ -166,3 +166,20 @@ def test_gpu_mass_conservation_and_two_edge_reduction():
     assert np.max(np.abs(r2[:n] - r1[:n])) < 1e-10
     assert np.max(np.abs(r2[n:][::-1] - r1[n:])) < 1e-10
     assert D > 0
+
+
+@pytest.mark.gpu
+def test_gpu_vs_oracle_high_degree_hub():
+    """A 64-edge hub (one vertex of degree 64) with linear drifts: the per-slot
+    exchange at a high-degree vertex, bit for bit against the C oracle."""
+    from oracle import oracle
+
+    g, f = build("hub64", gs)
+    grid = gs.EdgeGrid.uniform(g, 5)
+    dt = 0.8 * fvm.stability_limit(g, f, grid)
+    rho0 = np.random.default_rng(9).random(grid.n_cells)
+    p = fvm._pack(g, f, grid)
+    ref, n_ref = oracle.fvm_steps(rho0, 300, dt, p.reference_tuple())
+    got, n = fvm.fvm_steps_device(g, f, grid, rho0, 300, dt)
+    assert n == n_ref == 0
+    assert np.array_equal(got, ref)
