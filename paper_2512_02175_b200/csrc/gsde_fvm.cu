@@ -188,26 +188,30 @@ __global__ void __launch_bounds__(kFvmThreads)
   if (*(volatile int64_t *)neg_step) return;  // an earlier step went negative
   const int64_t step = (int64_t)red[3];
   const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+  // item order: the serial vertices, then vertex slots (the long items start
+  // first), then cells
   const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_ser = d.n_vser > 0 ? 1 : 0;
   double amax = 0.0, nmin = 0.0;  // max |rho|, max(-rho) over the cells written here
-  if (it < d.n_cells) {
-    if (!(d.cell_flags[it] & kOwned)) {
-      const double v = f.base(it);
-      f.out[it] = v;
-      track(v, amax, nmin);
-    }
-  } else if (it < d.n_cells + d.n_pslot) {
-    const int64_t sl = d.pslot[it - d.n_cells];
-    const int64_t v = d.slot_vertex[sl];
-    const double val = slot_update(f, v, (int)(sl - d.v_off[v]));
-    f.out[d.v_cells[sl]] = val;
-    track(val, amax, nmin);
-  } else if (it == d.n_cells + d.n_pslot && d.n_vser > 0) {
+  if (it < n_ser) {
     for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
     for (int64_t k = 0; k < d.n_vser; ++k) f.vertex_global(d.vser[k]);
     for (int64_t k = 0; k < d.n_vser; ++k)
       for (int64_t i = d.v_off[d.vser[k]]; i < d.v_off[d.vser[k] + 1]; ++i)
         track(f.out[d.v_cells[i]], amax, nmin);
+  } else if (it < n_ser + d.n_pslot) {
+    const int64_t sl = d.pslot[it - n_ser];
+    const int64_t v = d.slot_vertex[sl];
+    const double val = slot_update(f, v, (int)(sl - d.v_off[v]));
+    f.out[d.v_cells[sl]] = val;
+    track(val, amax, nmin);
+  } else if (it < n_ser + d.n_pslot + d.n_cells) {
+    const int64_t c = it - n_ser - d.n_pslot;
+    if (!(d.cell_flags[c] & kOwned)) {
+      const double v = f.base(c);
+      f.out[c] = v;
+      track(v, amax, nmin);
+    }
   }
   __shared__ double s_amax[kFvmThreads / 32], s_nmin[kFvmThreads / 32];
   __shared__ bool s_last;
@@ -268,7 +272,38 @@ cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int
   unsigned long long *r = reinterpret_cast<unsigned long long *>(red);
   const int64_t items = d.n_cells + d.n_pslot + (d.n_vser > 0 ? 1 : 0);
   const unsigned grid = (unsigned)((items + kFvmThreads - 1) / kFvmThreads);
-  for (int64_t k = 0; k < n_steps; ++k) {
+  // the step kernels are identical (the step index lives in red[3]), so runs of
+  // kGraphSteps launches are captured once into a CUDA graph and replayed;
+  // the remainder (or a stream the caller is already capturing) launches directly
+  constexpr int64_t kGraphSteps = 64;
+  int64_t left = n_steps;
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  err = cudaStreamIsCapturing(s, &cap_status);
+  if (err != cudaSuccess) return err;
+  if (n_steps >= 2 * kGraphSteps && cap_status == cudaStreamCaptureStatusNone) {
+    // capture on a private stream (the caller's may be the legacy default stream,
+    // which cannot capture), replay on the caller's
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cs = nullptr;
+    err = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (err != cudaSuccess) return err;
+    err = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (err == cudaSuccess) {
+      for (int64_t k = 0; k < kGraphSteps; ++k)
+        fvm_step_kernel<<<grid, kFvmThreads, 0, cs>>>(d, rho, scratch, dt, neg_floor, neg_step,
+                                                      r);
+      err = cudaStreamEndCapture(cs, &graph);
+    }
+    cudaStreamDestroy(cs);
+    if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
+    for (; err == cudaSuccess && left >= kGraphSteps; left -= kGraphSteps)
+      err = cudaGraphLaunch(exec, s);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (err != cudaSuccess) return err;
+  }
+  for (; left > 0; --left) {
     fvm_step_kernel<<<grid, kFvmThreads, 0, s>>>(d, rho, scratch, dt, neg_floor, neg_step, r);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
