@@ -352,10 +352,10 @@ def flush_l2(buf):
     buf.fill_(1)  # 256 MiB write > 126 MB L2
 
 
-# FVM step, algorithmic bytes per cell: read rho[c] (8) + the face drift shared
-# with the neighbour (8) + cell->edge (8) + owned flag (1), write new[c] (8);
-# neighbour densities and per-edge constants are L1 hits.
-FVM_BYTES_PER_CELL_STEP = 33
+# FVM step, algorithmic bytes per cell: read rho[c] (8) + the per-cell record
+# (left / right face drift, D, dx: 32; flags: 1), write new[c] (8); the
+# neighbour densities are L1 hits.
+FVM_BYTES_PER_CELL_STEP = 49
 
 
 def lane_ops_per_pstep(crossings_per_pstep):
