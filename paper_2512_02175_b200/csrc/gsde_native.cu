@@ -43,7 +43,9 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kMinBlocks = GSDE_MIN_BLOCKS;  // 4: caps registers at 64 -> 32 warps / SM
 constexpr int kMinBlocksStar = 3;            // star-graph ensembles: <= 85 registers
-constexpr int kMinBlocksTrials = 5;  // trials carry less state: <= 51 registers -> 40 warps / SM
+// trials: the compiler settles at 40 registers (48 warps / SM) under a 64-register
+// bound; the same kernel scheduled under a 51-register bound (5 blocks) ran 3% slower
+constexpr int kMinBlocksTrials = 4;
 constexpr int kPriv = 8;       // lane-private M-histogram bins
 constexpr int kTrips = 14;     // ensemble: trips per iteration
 constexpr uint32_t kDomainEnsemble = 0u;
