@@ -200,7 +200,7 @@ int gsde_histogram(int64_t n, const int64_t *edge, const double *x, const int64_
  * slot), vser (ascending) the other degree >= 2 vertices (cells shared
  * through single-cell edges), processed in vertex order by one thread. */
 typedef struct {
-  int64_t n_edges, n_cells, n_vertices, n_pslot, n_vser;
+  int64_t n_edges, n_cells, n_vertices, n_pslot, n_vser, n_terms;
   const double *cell_mu_l;   /* [C] drift on the left face (0 if none) */
   const double *cell_mu_r;   /* [C] drift on the right face (0 if none) */
   const double *cell_D;      /* [C] */
@@ -215,6 +215,14 @@ typedef struct {
   const int64_t *slot_vertex; /* [S] vertex of each slot */
   const int64_t *pslot;      /* [n_pslot] slots of the vertices whose cells no other vertex touches */
   const int64_t *vser;       /* [n_vser] the other degree >= 2 vertices, ascending */
+  /* two-phase exchange (fvm._term_layout): cell of pslot[t] sums the signed terms
+   * terms[tstart[t] .. tstart[t+1]) in the reference's order; exchange row pslot[t]
+   * writes its (j-side, i-side) term pairs to the positions rpos[rstart[t] ..
+   * rstart[t+1]) */
+  const int64_t *tstart;     /* [n_pslot+1] */
+  const int64_t *rstart;     /* [n_pslot+1] */
+  const int64_t *rpos;       /* [rstart[n_pslot]] */
+  double *terms;             /* [n_terms] device workspace */
 } gsde_fvm_desc;
 
 /* fvm_run's stepper (_fvm_step_loop, fvm.py:254-340): n_steps explicit Euler
@@ -223,8 +231,9 @@ typedef struct {
  * FP64).  After each step the run stops if min(0, min rho) <
  * neg_floor * max(1, max |rho|); *neg_step (device int64) receives the
  * 1-based step index, 0 if none.  red: caller-owned device scratch of 8
- * uint64.  One kernel per step (one thread per cell / vertex slot), all
- * stream-ordered; the stop test runs in the last block of each step. */
+ * uint64.  Two kernels per step (exchange terms per vertex slot, then one
+ * thread per cell / slot summing them), stream-ordered and replayed from a CUDA
+ * graph; the stop test runs in the last block of each step. */
 int gsde_fvm_run(const gsde_fvm_desc *d, double *rho, double *scratch, int64_t n_steps,
                  double dt, double neg_floor, int64_t *neg_step, uint64_t *red, void *stream);
 

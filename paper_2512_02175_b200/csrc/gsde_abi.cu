@@ -464,7 +464,9 @@ int gsde_fvm_run(const gsde_fvm_desc *d, double *rho, double *scratch, int64_t n
   if (!d || !rho || !scratch || !neg_step || !red || n_steps < 0 || !(dt > 0.0) ||
       d->n_edges < 1 || d->n_cells < 1 || d->n_vertices < 0 || d->n_pslot < 0 || d->n_vser < 0 ||
       !d->cell_mu_l || !d->cell_mu_r || !d->cell_D || !d->cell_dx || !d->cell_flags ||
-      !d->v_off || (d->n_pslot && (!d->pslot || !d->slot_vertex)) || (d->n_vser && !d->vser))
+      !d->v_off || (d->n_pslot && (!d->pslot || !d->slot_vertex || !d->tstart ||
+                                   !d->rstart || !d->rpos || (d->n_terms && !d->terms))) ||
+      (d->n_vser && !d->vser))
     return set_error(GSDE_EINVAL, "fvm_run: bad arguments");
   if (n_steps == 0) {
     const cudaError_t err = cudaMemsetAsync(neg_step, 0, sizeof(int64_t), (cudaStream_t)stream);

@@ -1,13 +1,16 @@
 // gsde_fvm.cu -- finite-volume Fokker-Planck baseline (reference fvm.py) on the GPU.
 //
-// One kernel per explicit Euler step, one thread per work item, every item
-// writing a disjoint set of cells of the next density:
+// Two kernels per explicit Euler step (exchange terms, then the update), one
+// thread per work item, every update item writing a disjoint set of cells of
+// the next density:
 //   * a cell not adjacent to a degree >= 2 vertex: rho +- its two interior
 //     face fluxes (per-cell SoA records: face drifts, D, dx -- one level of
 //     independent, coalesced loads);
 //   * a slot of a vertex whose adjacent cells no other vertex touches: the
-//     slot cell's face terms, then the contributions of the vertex exchange
-//     to that cell in the reference's loop order (O(degree) per thread);
+//     slot cell's face terms, then the exchange terms of that cell in the
+//     reference's loop order -- computed by the step's first kernel, one
+//     thread per exchange row (fvm_terms_kernel), so no thread carries a
+//     vertex's O(degree^2) chain of divisions;
 //   * one item for the remaining vertices (cells shared through single-cell
 //     edges): the same, one vertex after another in ascending order.
 // Every cell therefore sees the same sequence of IEEE operations as in
@@ -123,98 +126,55 @@ __device__ __forceinline__ void track(double v, double &amax, double &nmin) {
   nmin = fmax(nmin, -v);
 }
 
-// New density of the cell of slot k of vertex v (cells of v touched by no
-// other vertex): its face terms, then exactly the contributions the
-// reference's exchange loop (fvm.py:305-328) adds to THIS cell, in loop order.
-// Terms are recomputed per slot (the same IEEE operations as the serial loop),
-// so one vertex's slots update in parallel: O(deg) per thread, not O(deg^2).
-__device__ double slot_update(const Fvm &f, int64_t v, int k) {
+// Phase A of the vertex exchange: row i of vertex v (fvm.py:305-328) -- drift
+// exports i -> j and the diffusion pairs (i, j > i) -- written as signed terms
+// to the positions the destinations read them from (fvm._term_layout).  Every
+// term is the reference's own expression; a subtraction is stored negated.
+__device__ void exchange_row(const Fvm &f, int64_t t) {
   const gsde_fvm_desc &d = f.d;
+  const int64_t sl = d.pslot[t];
+  const int64_t v = d.slot_vertex[sl];
   const int64_t lo = d.v_off[v];
-  const int n = (int)(d.v_off[v + 1] - lo);
-  const double *b = d.v_b + lo, *dx = d.v_dx + lo, *sp = d.v_speed_in + lo, *Dd = d.v_D + lo;
+  const int n = (int)(d.v_off[v + 1] - lo), i = (int)(sl - lo);
+  const double *b = d.v_b + lo, *dx = d.v_dx + lo, *Dd = d.v_D + lo;
   const int64_t *cell = d.v_cells + lo;
-  const double dt = f.dt;
-  double acc = f.base(cell[k]);
-  const double bk = b[k], dxk = dx[k], rk = f.rho[cell[k]];
-  for (int i = 0; i < n; ++i) {
-    const double bi = b[i];
-    const double rho_i = i == k ? rk : f.rho[cell[i]];
-    if (sp[i] > 0.0) {
-      const double others = 1.0 - bi;
-      if (others > 0.0) {
-        const double total = sp[i] * rho_i;
-        if (i == k) {  // cell i exports to every other slot, in j order
-          for (int j = 0; j < n; ++j) {
-            if (j == i) continue;
-            const double fl = total * b[j] / others;
-            acc -= dt * fl / dxk;
-          }
-        } else {  // cell k receives its share once
-          const double fl = total * bk / others;
-          acc += dt * fl / dxk;
-        }
-      }
-    }
-    if (i > k) continue;  // pairs (i, j > i) touching k need i <= k
-    const double conc_i = rho_i / bi;
-    for (int j = (i == k ? i + 1 : k); j < (i == k ? n : k + 1); ++j) {
-      const double dpair = 0.5 * (Dd[i] + Dd[j]);
-      const double dxh = 2.0 * dx[i] * dx[j] / (dx[i] + dx[j]);
-      const double rj = j == k ? rk : f.rho[cell[j]];
-      const double g = dpair * (conc_i - rj / b[j]) / dxh;
-      if (g >= 0.0) {
-        const double fl = g * b[j];
-        if (j == k)
-          acc += dt * fl / dx[j];
-        else
-          acc -= dt * fl / dx[i];
-      } else {
-        const double fl = -g * b[i];
-        if (i == k)
-          acc += dt * fl / dx[i];
-        else
-          acc -= dt * fl / dx[j];
-      }
+  const int64_t *pos = d.rpos + d.rstart[t];
+  const double dt = f.dt, bi = b[i], dxi = dx[i], rho_i = f.rho[cell[i]];
+  const double sp = d.v_speed_in[sl], others = 1.0 - bi;
+  if (sp > 0.0 && others > 0.0) {
+    const double total = sp * rho_i;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double fl = total * b[j] / others;
+      d.terms[pos[0]] = dt * fl / dx[j];
+      d.terms[pos[1]] = -(dt * fl / dxi);
+      pos += 2;
     }
   }
-  return acc;
+  const double conc_i = rho_i / bi;
+  for (int j = i + 1; j < n; ++j) {
+    const double dpair = 0.5 * (Dd[i] + Dd[j]);
+    const double dxh = 2.0 * dxi * dx[j] / (dxi + dx[j]);
+    const double g = dpair * (conc_i - f.rho[cell[j]] / b[j]) / dxh;
+    if (g >= 0.0) {
+      const double fl = g * b[j];
+      d.terms[pos[0]] = dt * fl / dx[j];
+      d.terms[pos[1]] = -(dt * fl / dxi);
+    } else {
+      const double fl = -g * bi;
+      d.terms[pos[1]] = dt * fl / dxi;
+      d.terms[pos[0]] = -(dt * fl / dx[j]);
+    }
+    pos += 2;
+  }
 }
 
-// 6 blocks / SM (40 registers): the step is latency-bound, resident warps
-// beat the few spills of the vertex-slot path (+8% over 64 registers)
-__global__ void __launch_bounds__(kFvmThreads, 6)
-    fvm_step_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
-                    double dt, double neg_floor, int64_t *neg_step,
-                    unsigned long long *red) {
-  if (*(volatile int64_t *)neg_step) return;  // an earlier step went negative
-  const int64_t step = (int64_t)red[3];
-  const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
-  // item order: the serial vertices, then vertex slots (the long items start
-  // first), then cells
-  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n_ser = d.n_vser > 0 ? 1 : 0;
-  double amax = 0.0, nmin = 0.0;  // max |rho|, max(-rho) over the cells written here
-  if (it < n_ser) {
-    for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
-    for (int64_t k = 0; k < d.n_vser; ++k) f.vertex_global(d.vser[k]);
-    for (int64_t k = 0; k < d.n_vser; ++k)
-      for (int64_t i = d.v_off[d.vser[k]]; i < d.v_off[d.vser[k] + 1]; ++i)
-        track(f.out[d.v_cells[i]], amax, nmin);
-  } else if (it < n_ser + d.n_pslot) {
-    const int64_t sl = d.pslot[it - n_ser];
-    const int64_t v = d.slot_vertex[sl];
-    const double val = slot_update(f, v, (int)(sl - d.v_off[v]));
-    f.out[d.v_cells[sl]] = val;
-    track(val, amax, nmin);
-  } else if (it < n_ser + d.n_pslot + d.n_cells) {
-    const int64_t c = it - n_ser - d.n_pslot;
-    if (!(d.cell_flags[c] & kOwned)) {
-      const double v = f.base(c);
-      f.out[c] = v;
-      track(v, amax, nmin);
-    }
-  }
+// Block max of (|rho|, -rho) over the cells a block wrote, folded into red[0..1]
+// with one pair of 64-bit atomics per block (bit patterns of non-negative doubles
+// order like the doubles).  Returns true in the block that finished last when
+// `count` is set (red[2] counts those blocks).
+__device__ __forceinline__ bool block_fold(double amax, double nmin, unsigned long long *red,
+                                           bool count) {
   __shared__ double s_amax[kFvmThreads / 32], s_nmin[kFvmThreads / 32];
   __shared__ bool s_last;
 #pragma unroll
@@ -232,16 +192,78 @@ __global__ void __launch_bounds__(kFvmThreads, 6)
       amax = fmax(amax, s_amax[w]);
       nmin = fmax(nmin, s_nmin[w]);
     }
-    // canonical +0: the bit-pattern max below orders non-negative doubles only
+    // canonical +0: the bit-pattern max orders non-negative doubles only
     amax = amax > 0.0 ? amax : 0.0;
     nmin = nmin > 0.0 ? nmin : 0.0;
-    atomicMax(&red[0], (unsigned long long)__double_as_longlong(amax));
-    atomicMax(&red[1], (unsigned long long)__double_as_longlong(nmin));
-    __threadfence();
-    s_last = atomicAdd(&red[2], 1ull) == gridDim.x - 1;
+    if (amax > 0.0) atomicMax(&red[0], (unsigned long long)__double_as_longlong(amax));
+    if (nmin > 0.0) atomicMax(&red[1], (unsigned long long)__double_as_longlong(nmin));
+    s_last = false;
+    if (count) {
+      __threadfence();
+      s_last = atomicAdd(&red[2], 1ull) == gridDim.x - 1;
+    }
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {  // every block's maxima are in: the stop test
+  return s_last;
+}
+
+// Phase 1 of a step: exchange rows (terms for phase 2) and every cell no vertex
+// owns (its final value).  One resident wave of blocks strides over
+// [rows | cells]; both kinds are independent, latency-bound work.
+__global__ void __launch_bounds__(kFvmThreads, 6)
+    fvm_phase1_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
+                      double dt, const int64_t *neg_step, unsigned long long *red) {
+  if (*(volatile const int64_t *)neg_step) return;  // an earlier step went negative
+  const int64_t step = (int64_t)red[3];
+  const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+  const int64_t n_items = d.n_pslot + d.n_cells;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double amax = 0.0, nmin = 0.0;  // max |rho|, max(-rho) over the cells written here
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += stride) {
+    if (it < d.n_pslot) {
+      exchange_row(f, it);
+    } else {
+      const int64_t c = it - d.n_pslot;
+      if (!(d.cell_flags[c] & kOwned)) {
+        const double v = f.base(c);
+        f.out[c] = v;
+        track(v, amax, nmin);
+      }
+    }
+  }
+  block_fold(amax, nmin, red, false);
+}
+
+// Phase 2: vertex-adjacent cells (face terms + their exchange terms in the
+// reference's order), the serial vertices, and the stop test in the last block.
+__global__ void __launch_bounds__(kFvmThreads, 6)
+    fvm_phase2_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
+                      double dt, double neg_floor, int64_t *neg_step,
+                      unsigned long long *red) {
+  if (*(volatile int64_t *)neg_step) return;
+  const int64_t step = (int64_t)red[3];
+  const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+  const int64_t n_ser = d.n_vser > 0 ? 1 : 0;
+  const int64_t n_items = n_ser + d.n_pslot;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double amax = 0.0, nmin = 0.0;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += stride) {
+    if (it < n_ser) {
+      for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
+      for (int64_t k = 0; k < d.n_vser; ++k) f.vertex_global(d.vser[k]);
+      for (int64_t k = 0; k < d.n_vser; ++k)
+        for (int64_t i = d.v_off[d.vser[k]]; i < d.v_off[d.vser[k] + 1]; ++i)
+          track(f.out[d.v_cells[i]], amax, nmin);
+    } else {
+      const int64_t t = it - n_ser;
+      const int64_t c = d.v_cells[d.pslot[t]];
+      double val = f.base(c);
+      for (int64_t m = d.tstart[t]; m < d.tstart[t + 1]; ++m) val += d.terms[m];
+      f.out[c] = val;
+      track(val, amax, nmin);
+    }
+  }
+  if (block_fold(amax, nmin, red, true) && threadIdx.x == 0) {  // all maxima are in
     __threadfence();
     const volatile unsigned long long *vr = red;
     const double mx = fmax(1.0, __longlong_as_double((long long)vr[0]));
@@ -272,19 +294,36 @@ cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int
   if (err == cudaSuccess) err = cudaMemsetAsync(neg_step, 0, sizeof(int64_t), s);
   if (err != cudaSuccess) return err;
   unsigned long long *r = reinterpret_cast<unsigned long long *>(red);
-  const int64_t items = d.n_cells + d.n_pslot + (d.n_vser > 0 ? 1 : 0);
-  const unsigned grid = (unsigned)((items + kFvmThreads - 1) / kFvmThreads);
+  int device = 0;
+  cudaGetDevice(&device);
+  int per1 = 0, per2 = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, fvm_phase1_kernel, kFvmThreads, 0);
+  if (err == cudaSuccess)
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fvm_phase2_kernel, kFvmThreads, 0);
+  if (err != cudaSuccess) return err;
+  const int64_t sms = dev_info(device).sm_count;
+  auto wave = [&](int64_t items, int per) {
+    const int64_t need = (items + kFvmThreads - 1) / kFvmThreads;
+    const int64_t w = sms * (per > 0 ? per : 1);
+    return (unsigned)(need < 1 ? 1 : (need < w ? need : w));
+  };
+  const unsigned g1 = wave(d.n_pslot + d.n_cells, per1);
+  const unsigned g2 = wave((d.n_vser > 0 ? 1 : 0) + d.n_pslot, per2);
+  auto step = [&](cudaStream_t st) {
+    fvm_phase1_kernel<<<g1, kFvmThreads, 0, st>>>(d, rho, scratch, dt, neg_step, r);
+    fvm_phase2_kernel<<<g2, kFvmThreads, 0, st>>>(d, rho, scratch, dt, neg_floor, neg_step, r);
+  };
   // the step kernels are identical (the step index lives in red[3]), so runs of
-  // kGraphSteps launches are captured once into a CUDA graph and replayed;
-  // the remainder (or a stream the caller is already capturing) launches directly
+  // kGraphSteps steps are captured once into a CUDA graph and replayed; the
+  // remainder (or a stream the caller is already capturing) launches directly
   constexpr int64_t kGraphSteps = 64;
   int64_t left = n_steps;
   cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
   err = cudaStreamIsCapturing(s, &cap_status);
   if (err != cudaSuccess) return err;
   if (n_steps >= 2 * kGraphSteps && cap_status == cudaStreamCaptureStatusNone) {
-    // capture on a private stream (the caller's may be the legacy default stream,
-    // which cannot capture), replay on the caller's
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot capture), replay on the caller's
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaStream_t cs = nullptr;
@@ -292,9 +331,7 @@ cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int
     if (err != cudaSuccess) return err;
     err = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
     if (err == cudaSuccess) {
-      for (int64_t k = 0; k < kGraphSteps; ++k)
-        fvm_step_kernel<<<grid, kFvmThreads, 0, cs>>>(d, rho, scratch, dt, neg_floor, neg_step,
-                                                      r);
+      for (int64_t k = 0; k < kGraphSteps; ++k) step(cs);
       err = cudaStreamEndCapture(cs, &graph);
     }
     cudaStreamDestroy(cs);
@@ -306,13 +343,11 @@ cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int
     if (err != cudaSuccess) return err;
   }
   for (; left > 0; --left) {
-    fvm_step_kernel<<<grid, kFvmThreads, 0, s>>>(d, rho, scratch, dt, neg_floor, neg_step, r);
+    step(s);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
-  count_launch((int)(n_steps < (1 << 30) ? n_steps : (1 << 30)));
-  int device = 0;
-  cudaGetDevice(&device);
+  count_launch((int)(n_steps < (1 << 29) ? 2 * n_steps : (1 << 30)));
   const int64_t blocks = (d.n_cells + kFvmThreads - 1) / kFvmThreads;
   const int64_t cap = (int64_t)dev_info(device).sm_count * 8;
   fvm_finish_kernel<<<(unsigned)(blocks < cap ? blocks : cap), kFvmThreads, 0, s>>>(

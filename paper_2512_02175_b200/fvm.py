@@ -192,6 +192,12 @@ class _Packed:
     vser: np.ndarray
     slot_vertex: np.ndarray
     pslot: np.ndarray
+    # two-phase vertex exchange (see _term_layout): destination ranges per pslot
+    # entry, per-row write positions, and the number of terms
+    tstart: np.ndarray
+    rstart: np.ndarray
+    rpos: np.ndarray
+    n_terms: int
     # per-cell records of the GPU stepper: drift on the left / right interior
     # face, D and dx of the cell's edge, flags (1 left face, 2 right face, 4 owned)
     cell_mu_l: np.ndarray
@@ -242,6 +248,8 @@ def _pack(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> _Packe
     shared = np.zeros(deg.shape[0], dtype=bool)
     shared[np.unique(slot_vertex[multi & (owners[v_cells] >= 2)])] = True
     hub = deg >= 2
+    pslot = np.flatnonzero((hub & ~shared)[slot_vertex]).astype(np.int64)
+    tstart, rstart, rpos, n_terms = _term_layout(v_off, v_b, v_speed_in, pslot, slot_vertex)
     cell_edge = np.repeat(np.arange(E, dtype=np.int64), counts)
     local = np.arange(n_cells, dtype=np.int64) - offs[cell_edge]
     left = local > 0
@@ -261,10 +269,75 @@ def _pack(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> _Packe
         cell_edge=cell_edge, owned=owned.astype(np.uint8),
         vpar=np.flatnonzero(hub & ~shared).astype(np.int64),
         vser=np.flatnonzero(hub & shared).astype(np.int64),
-        slot_vertex=slot_vertex,
-        pslot=np.flatnonzero((hub & ~shared)[slot_vertex]).astype(np.int64),
+        slot_vertex=slot_vertex, pslot=pslot, tstart=tstart, rstart=rstart, rpos=rpos,
+        n_terms=n_terms,
         cell_mu_l=cell_mu_l, cell_mu_r=cell_mu_r, cell_D=D_edge[cell_edge].copy(),
         cell_dx=dx[cell_edge].copy(), cell_flags=flags.astype(np.uint8))
+
+
+def _term_layout(v_off, v_b, v_speed_in, pslot, slot_vertex):
+    """Static layout of the two-phase vertex exchange on the GPU.
+
+    Every contribution the reference's exchange loop (``fvm.py:305-328``) adds to
+    a vertex-adjacent cell is one signed *term*.  Phase A (one thread per slot
+    i = exchange *row*) computes row i's terms -- drift exports i -> j and the
+    diffusion pairs (i, j > i) -- and writes each to its position; phase B (one
+    thread per slot k) adds the terms of cell k in exactly the order the
+    reference applies them:
+
+        for i in 0..n-1:
+            drift row i (sp_i > 0 and 1 - b_i > 0):  i == k: -(dt f_ij / dx_i) for j != k
+                                                      i != k: +(dt f_ik / dx_k)
+            diffusion:  i < k: pair (i, k), k's share;  i == k: pairs (k, j > k), k's share
+
+    so a - b is added as a + (-b), bit-identical.  Returns (tstart, rstart,
+    rpos, n_terms): cell k's terms are ``T[tstart[t]:tstart[t+1]]`` (t = its
+    index in ``pslot``); row t writes its j-side / i-side pairs to
+    ``rpos[rstart[t]:rstart[t+1]]``."""
+    n_p = pslot.shape[0]
+    tstart = np.zeros(n_p + 1, dtype=np.int64)
+    rstart = np.zeros(n_p + 1, dtype=np.int64)
+    rpos_parts = []
+    pos = 0
+    t = 0
+    while t < n_p:
+        v = int(slot_vertex[pslot[t]])
+        lo, n = int(v_off[v]), int(v_off[v + 1] - v_off[v])
+        active = [(v_speed_in[lo + i] > 0.0) and (1.0 - v_b[lo + i] > 0.0) for i in range(n)]
+        where = {}
+        for k in range(n):
+            tstart[t + k] = pos
+            for i in range(n):
+                if active[i]:
+                    if i == k:
+                        for j in range(n):
+                            if j != k:
+                                where[("o", i, j)] = pos
+                                pos += 1
+                    else:
+                        where[("n", i, k)] = pos
+                        pos += 1
+                if i < k:
+                    where[("j", i, k)] = pos
+                    pos += 1
+                elif i == k:
+                    for j in range(k + 1, n):
+                        where[("i", k, j)] = pos
+                        pos += 1
+        for i in range(n):
+            rows = []
+            if active[i]:
+                for j in range(n):
+                    if j != i:
+                        rows += [where[("n", i, j)], where[("o", i, j)]]
+            for j in range(i + 1, n):
+                rows += [where[("j", i, j)], where[("i", i, j)]]
+            rstart[t + i + 1] = rstart[t + i] + len(rows)
+            rpos_parts.append(np.asarray(rows, dtype=np.int64))
+        t += n
+    tstart[n_p] = pos
+    rpos = np.concatenate(rpos_parts) if rpos_parts else np.zeros(0, dtype=np.int64)
+    return tstart, rstart, rpos, pos
 
 
 def stability_limit(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> float:
@@ -302,14 +375,16 @@ def stability_limit(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid)
 
 
 _DESC_ARRAYS = ("cell_mu_l", "cell_mu_r", "cell_D", "cell_dx", "cell_flags", "v_off", "v_cells",
-                "v_b", "v_dx", "v_speed_in", "v_D", "slot_vertex", "pslot", "vser")
+                "v_b", "v_dx", "v_speed_in", "v_D", "slot_vertex", "pslot", "vser", "tstart",
+                "rstart", "rpos")
 
 
 class _Desc(C.Structure):
     """``gsde_fvm_desc`` (include/gsde.h)."""
 
-    _fields_ = [(n, C.c_int64) for n in ("n_edges", "n_cells", "n_vertices", "n_pslot", "n_vser")] + [
-        (n, C.c_void_p) for n in _DESC_ARRAYS]
+    _fields_ = [(n, C.c_int64) for n in ("n_edges", "n_cells", "n_vertices", "n_pslot", "n_vser",
+                                         "n_terms")] + [
+        (n, C.c_void_p) for n in _DESC_ARRAYS + ("terms",)]
 
 
 def _device_pack(p: _Packed, n_vertices: int, device: int):
@@ -319,11 +394,14 @@ def _device_pack(p: _Packed, n_vertices: int, device: int):
     d = _Desc()
     d.n_edges, d.n_cells = p.dx_edge.shape[0], p.cell_edge.shape[0]
     d.n_vertices, d.n_pslot, d.n_vser = n_vertices, p.pslot.shape[0], p.vser.shape[0]
+    d.n_terms = p.n_terms
     for name in _DESC_ARRAYS:
         a = getattr(p, name)
         t = torch.from_numpy(np.ascontiguousarray(a) if a.size else np.zeros(1, a.dtype)).to(**kw)
         keep[name] = t
         setattr(d, name, t.data_ptr())
+    keep["terms"] = torch.empty(max(1, p.n_terms), dtype=torch.float64, **kw)  # workspace
+    d.terms = keep["terms"].data_ptr()
     return d, keep, torch, dev
 
 
