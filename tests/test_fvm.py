@@ -183,3 +183,24 @@ def test_gpu_vs_oracle_high_degree_hub():
     got, n = fvm.fvm_steps_device(g, f, grid, rho0, 300, dt)
     assert n == n_ref == 0
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["hub8", "general_ragged", "star4_mixed_pos"])
+def test_term_layout_is_a_permutation(name):
+    """Every exchange term has exactly one writer row and one reader cell."""
+    g, f, grid, *_ = setup(name)
+    p = fvm._pack(g, f, grid)
+    assert p.tstart[0] == 0 and p.tstart[-1] == p.n_terms
+    assert np.all(np.diff(p.tstart) >= 0)
+    written = np.sort(p.rpos)
+    assert np.array_equal(written, np.arange(p.n_terms))  # each position written once
+    # a cell of degree-n vertex receives: its n-1 own exports if active, one share of every
+    # other active row, and one term per diffusion pair it belongs to (n-1)
+    for t, sl in enumerate(p.pslot):
+        v = p.slot_vertex[sl]
+        lo, hi = p.v_off[v], p.v_off[v + 1]
+        n = hi - lo
+        active = (p.v_speed_in[lo:hi] > 0) & (1.0 - p.v_b[lo:hi] > 0)
+        k = sl - lo
+        want = (n - 1) * active[k] + (active.sum() - active[k]) + (n - 1)
+        assert p.tstart[t + 1] - p.tstart[t] == want
