@@ -55,15 +55,15 @@ struct Fvm {
   // rho[c] plus its interior-face terms in the reference's order:
   // new[c] += scale F(left face), then new[c] -= scale F(right face)
   __device__ __forceinline__ double base(int64_t c) const {
-    const uint8_t fl = d.cell_flags[c];
-    const double D = d.cell_D[c], dx = d.cell_dx[c];
-    const double rc = rho[c];
-    const double rl = (fl & kLeft) ? rho[c - 1] : 0.0;
-    const double rr = (fl & kRight) ? rho[c + 1] : 0.0;
+    const uint8_t fl = __ldg(d.cell_flags + c);
+    const double D = __ldg(d.cell_D + c), dx = __ldg(d.cell_dx + c);
+    const double rc = __ldg(rho + c);
+    const double rl = (fl & kLeft) ? __ldg(rho + c - 1) : 0.0;
+    const double rr = (fl & kRight) ? __ldg(rho + c + 1) : 0.0;
     const double scale = dt / dx;
     double v = rc;
-    if (fl & kLeft) v += scale * face(d.cell_mu_l[c], D, dx, rl, rc);
-    if (fl & kRight) v -= scale * face(d.cell_mu_r[c], D, dx, rc, rr);
+    if (fl & kLeft) v += scale * face(__ldg(d.cell_mu_l + c), D, dx, rl, rc);
+    if (fl & kRight) v -= scale * face(__ldg(d.cell_mu_r + c), D, dx, rc, rr);
     return v;
   }
 
@@ -131,39 +131,47 @@ __device__ __forceinline__ void track(double v, double &amax, double &nmin) {
 // to the positions the destinations read them from (fvm._term_layout).  Every
 // term is the reference's own expression; a subtraction is stored negated.
 __device__ void exchange_row(const Fvm &f, int64_t t) {
+  // every input is read-only during the step: __ldg lets the loads of later
+  // iterations run ahead of this row's term stores
   const gsde_fvm_desc &d = f.d;
-  const int64_t sl = d.pslot[t];
-  const int64_t v = d.slot_vertex[sl];
-  const int64_t lo = d.v_off[v];
-  const int n = (int)(d.v_off[v + 1] - lo), i = (int)(sl - lo);
+  const int64_t sl = __ldg(d.pslot + t);
+  const int64_t v = __ldg(d.slot_vertex + sl);
+  const int64_t lo = __ldg(d.v_off + v);
+  const int n = (int)(__ldg(d.v_off + v + 1) - lo), i = (int)(sl - lo);
   const double *b = d.v_b + lo, *dx = d.v_dx + lo, *Dd = d.v_D + lo;
   const int64_t *cell = d.v_cells + lo;
-  const int64_t *pos = d.rpos + d.rstart[t];
-  const double dt = f.dt, bi = b[i], dxi = dx[i], rho_i = f.rho[cell[i]];
-  const double sp = d.v_speed_in[sl], others = 1.0 - bi;
+  const int64_t *pos = d.rpos + __ldg(d.rstart + t);
+  const double dt = f.dt, bi = __ldg(b + i), dxi = __ldg(dx + i), Di = __ldg(Dd + i);
+  const double rho_i = __ldg(f.rho + __ldg(cell + i));
+  const double sp = __ldg(d.v_speed_in + sl), others = 1.0 - bi;
   if (sp > 0.0 && others > 0.0) {
     const double total = sp * rho_i;
     for (int j = 0; j < n; ++j) {
       if (j == i) continue;
-      const double fl = total * b[j] / others;
-      d.terms[pos[0]] = dt * fl / dx[j];
-      d.terms[pos[1]] = -(dt * fl / dxi);
+      const double fl = total * __ldg(b + j) / others;
+      const int64_t p0 = __ldg(pos), p1 = __ldg(pos + 1);
+      d.terms[p0] = dt * fl / __ldg(dx + j);
+      d.terms[p1] = -(dt * fl / dxi);
       pos += 2;
     }
   }
   const double conc_i = rho_i / bi;
+#pragma unroll 2
   for (int j = i + 1; j < n; ++j) {
-    const double dpair = 0.5 * (Dd[i] + Dd[j]);
-    const double dxh = 2.0 * dxi * dx[j] / (dxi + dx[j]);
-    const double g = dpair * (conc_i - f.rho[cell[j]] / b[j]) / dxh;
+    const double bj = __ldg(b + j), dxj = __ldg(dx + j);
+    const double rj = __ldg(f.rho + __ldg(cell + j));
+    const int64_t p0 = __ldg(pos), p1 = __ldg(pos + 1);
+    const double dpair = 0.5 * (Di + __ldg(Dd + j));
+    const double dxh = 2.0 * dxi * dxj / (dxi + dxj);
+    const double g = dpair * (conc_i - rj / bj) / dxh;
     if (g >= 0.0) {
-      const double fl = g * b[j];
-      d.terms[pos[0]] = dt * fl / dx[j];
-      d.terms[pos[1]] = -(dt * fl / dxi);
+      const double fl = g * bj;
+      d.terms[p0] = dt * fl / dxj;
+      d.terms[p1] = -(dt * fl / dxi);
     } else {
       const double fl = -g * bi;
-      d.terms[pos[1]] = dt * fl / dxi;
-      d.terms[pos[0]] = -(dt * fl / dx[j]);
+      d.terms[p1] = dt * fl / dxi;
+      d.terms[p0] = -(dt * fl / dxj);
     }
     pos += 2;
   }
@@ -210,7 +218,9 @@ __device__ __forceinline__ bool block_fold(double amax, double nmin, unsigned lo
 // Phase 1 of a step: exchange rows (terms for phase 2) and every cell no vertex
 // owns (its final value).  One resident wave of blocks strides over
 // [rows | cells]; both kinds are independent, latency-bound work.
-__global__ void __launch_bounds__(kFvmThreads, 6)
+// phase kernels at 64 registers (4 blocks / SM): measured 4/4 72 ms, 4/6 74 ms,
+// 6/6 75 ms, 8/8 80 ms per 2000 C4 steps
+__global__ void __launch_bounds__(kFvmThreads, 4)
     fvm_phase1_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
                       double dt, const int64_t *neg_step, unsigned long long *red) {
   if (*(volatile const int64_t *)neg_step) return;  // an earlier step went negative
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(kFvmThreads, 6)
 
 // Phase 2: vertex-adjacent cells (face terms + their exchange terms in the
 // reference's order), the serial vertices, and the stop test in the last block.
-__global__ void __launch_bounds__(kFvmThreads, 6)
+__global__ void __launch_bounds__(kFvmThreads, 4)
     fvm_phase2_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
                       double dt, double neg_floor, int64_t *neg_step,
                       unsigned long long *red) {
