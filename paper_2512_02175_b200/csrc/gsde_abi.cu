@@ -220,7 +220,10 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   std::vector<int4> nedgev(E), ncol(S);
   for (int64_t e = 0; e < E; ++e) {
     float4 r;
+    // FP32 length rounded toward zero, so every native position (<= the FP32
+    // length) also lies within the reference's FP64 edge [0, l]
     r.x = len32[e];
+    if (std::isfinite(len64[e]) && (double)r.x > len64[e]) r.x = std::nextafter(r.x, 0.0f);
     r.w = sig32[e];
     if (kind[e] == 0) {
       r.y = coef32[e];

@@ -521,7 +521,7 @@ __device__ __forceinline__ void place_values(const NativeGraph &G, const Tables<
                                              const NatParams &p, uint64_t id, int &e, float &x) {
   if (p.init_kind == GSDE_INIT_POINT) {
     e = p.init_edge;
-    x = p.init_x;
+    x = fminf(p.init_x, T.E(e).x);  // the FP32 edge, like every native position
   } else {
     const Block r = native_block(p, 0u, kDomainPlace, id);
     const double u = (double)((((uint64_t)r.x << 32) | r.y) >> 11) * kInv2p53;

@@ -294,3 +294,42 @@ def test_pipelined_run_ensemble_equals_single_launch():
     np.testing.assert_array_equal(r.crossing_events, d["events"].cpu().numpy())
     np.testing.assert_array_equal(r.stats.m_histogram, d["m_hist"].cpu().numpy())
     assert r.stats.crossings_total == int(d["totals"][0])
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_native_invariants_random_graphs(seed):
+    """Randomised sweep of the native kernels (general and star graphs, random
+    dt / caps / initial laws): every final state lies on its edge, the fused
+    estimators agree with the per-particle outputs, nothing is NaN."""
+    rng = np.random.default_rng(5000 + seed)
+    if seed % 3 == 0:  # star: semi-infinite edges, random drifts toward / away from 0
+        k = int(rng.integers(2, 9))
+        spec = dict(edges=[(0, None, float("inf"))] * k, weights=None,
+                    drift=[("constant", float(rng.uniform(-30, 5))) for _ in range(k)],
+                    sigma=[float(rng.uniform(0.5, 2.0)) for _ in range(k)])
+    else:
+        spec = cases._random_general(int(rng.integers(4, 40)), int(rng.integers(0, 10)),
+                                     int(rng.integers(0, 1 << 30)))
+    g, f = cases.build(spec, gs)
+    dt = float(10 ** rng.uniform(-4, -2))
+    cap = int(rng.choice([1, 3, 100]))
+    n = int(rng.integers(1, 200_000))
+    xmax = 1.0 if g.is_star else float(np.max(g.edge_length))
+    cfg = gs.SimulationConfig(dt=dt, n_steps=int(rng.integers(0, 300)), n_particles=n,
+                              seed=seed, initial=gs.PerEdgeUniform(xmax),
+                              max_splits_per_step=cap)
+    lengths = g.edge_length if not g.is_star else np.full(g.n_edges, 5.0)
+    grid = gs.EdgeGrid.uniform(g, 4, lengths=lengths)
+    d = engine.ensemble_device(g, f, cfg, outputs=("all", "edge_counts"), grid=grid)
+    e, x = d["edge"].cpu().numpy(), d["x"].cpu().numpy()
+    assert e.min() >= 0 and e.max() < g.n_edges
+    assert np.all(np.isfinite(x)) and np.all(x >= 0.0)
+    assert np.all(x <= g.edge_length[e])
+    np.testing.assert_array_equal(d["edge_counts"].cpu().numpy(), np.bincount(e, minlength=g.n_edges))
+    assert int(d["hist"].sum()) == n
+    mh = d["m_hist"].cpu().numpy()
+    tot = d["totals"].cpu().numpy()
+    cr, ev = d["crossings"].cpu().numpy(), d["events"].cpu().numpy()
+    assert int(cr.sum()) == int(tot[0]) and int(ev.sum()) == int(tot[1])
+    assert int(mh.sum()) == int(tot[1])
+    assert int(d["truncs"].cpu().numpy().sum()) == int(tot[2])

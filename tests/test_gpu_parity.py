@@ -263,3 +263,33 @@ def test_occupation_reference_stream_matches_oracle(case, every, start, init):
                                      helpers.oracle_init(init, g))
     np.testing.assert_array_equal(h.counts, occ)
     assert h.total == 3000 * ((60 - start) // every) == int(occ.sum())
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_reference_stream_vs_oracle_random_graphs(seed):
+    """Randomised sweep: random connected graphs (tree + loops, mixed constant /
+    linear / tabulated drifts, non-uniform and zero jump weights, varying sigma),
+    random dt, caps and initial laws; edge ids, crossings, events and M
+    histograms exact vs the oracle, positions within POS_ATOL."""
+    rng = np.random.default_rng(1000 + seed)
+    spec = cases._random_general(int(rng.integers(4, 30)), int(rng.integers(0, 8)),
+                                 int(rng.integers(0, 1 << 30)))
+    g, f = cases.build(spec, gs)
+    dt = float(10 ** rng.uniform(-4, -2))
+    cap = int(rng.choice([1, 2, 5, 100]))
+    n, steps = 4000, int(rng.integers(20, 120))
+    if rng.random() < 0.5:
+        init = ("uniform", float(rng.uniform(0.2, 2.0)))
+    else:
+        e = int(rng.integers(0, g.n_edges))
+        init = ("point", e, float(rng.uniform(0.0, g.edge_length[e])))
+    cfg = gs.SimulationConfig(dt=dt, n_steps=steps, n_particles=n, seed=seed + 7,
+                              initial=helpers.initial_for(init), rng="reference",
+                              max_splits_per_step=cap)
+    r = gs.run_ensemble(g, f, cfg)
+    o = _oracle_run(g, f, seed + 7, n, steps, dt, helpers.oracle_init(init, g), cap)
+    np.testing.assert_array_equal(r.edges, o["edges"])
+    np.testing.assert_array_equal(r.crossings, o["crossings"])
+    np.testing.assert_array_equal(r.crossing_events, o["crossing_events"])
+    np.testing.assert_array_equal(r.stats.m_histogram, o["m_histogram"])
+    helpers.assert_positions(r.positions, o["positions"])
