@@ -293,3 +293,51 @@ def test_reference_stream_vs_oracle_random_graphs(seed):
     np.testing.assert_array_equal(r.crossing_events, o["crossing_events"])
     np.testing.assert_array_equal(r.stats.m_histogram, o["m_histogram"])
     helpers.assert_positions(r.positions, o["positions"])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_reference_stream_trials_vs_oracle_random(seed):
+    """Vertex trials from random vertices of random graphs (and random stars),
+    reference stream: M, exit edges and truncations exact vs the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    if seed % 2:
+        k = int(rng.integers(2, 9))
+        spec = dict(edges=[(0, None, float("inf"))] * k, weights=None,
+                    drift=[("constant", float(rng.uniform(-40, 5))) for _ in range(k)],
+                    sigma=[float(rng.uniform(0.5, 2.0)) for _ in range(k)])
+    else:
+        spec = cases._random_general(int(rng.integers(4, 25)), int(rng.integers(0, 6)),
+                                     int(rng.integers(0, 1 << 30)))
+    g, f = cases.build(spec, gs)
+    v = 0 if g.is_star else int(rng.integers(0, g.n_vertices))
+    dt = float(10 ** rng.uniform(-4, -1.5))
+    cap = int(rng.choice([2, 10, 100]))
+    tr = gs.vertex_crossing_trials(g, f, dt, 20_000, seed, vertex=v, max_splits=cap,
+                                   rng="reference")
+    e0, x0 = engine._trial_start(g, v)
+    o = oracle.vertex_trials(oracle.OracleGraph(g, f), seed, 20_000, dt, e0, x0, cap)
+    np.testing.assert_array_equal(tr.M, o["M"])
+    np.testing.assert_array_equal(tr.exit_edges, o["exit_edges"])
+    np.testing.assert_array_equal(tr.truncated, o["truncated"])
+    helpers.assert_positions(tr.exit_positions, o["exit_positions"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_native_vs_reference_stream_random_graphs(seed):
+    """Statistical parity on random graphs: final-edge occupancy and crossings
+    per step of the native stream agree with the reference stream
+    (two-sample chi-square, p > 1e-4 with 6 cases)."""
+    rng = np.random.default_rng(9000 + seed)
+    spec = cases._random_general(int(rng.integers(5, 20)), int(rng.integers(1, 5)),
+                                 int(rng.integers(0, 1 << 30)))
+    g, f = cases.build(spec, gs)
+    xmax = float(np.max(g.edge_length))
+    mk = lambda r, s: gs.SimulationConfig(dt=2e-3, n_steps=200, n_particles=400_000, seed=s,
+                                          initial=gs.PerEdgeUniform(xmax), rng=r)
+    a = engine.ensemble_device(g, f, mk("native", 1), outputs=("edge_counts",))
+    b = engine.ensemble_device(g, f, mk("reference", 2), outputs=("edge_counts",))
+    p, chi2, dof = helpers.chi2_two_sample(a["edge_counts"].cpu().numpy(),
+                                           b["edge_counts"].cpu().numpy())
+    assert p > 1e-4, (p, chi2, dof)
+    ca, cb = int(a["totals"][0]), int(b["totals"][0])
+    assert abs(ca - cb) < 5 * np.sqrt(ca + cb) + 0.01 * cb, (ca, cb)
