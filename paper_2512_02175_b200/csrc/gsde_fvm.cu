@@ -286,6 +286,81 @@ __global__ void __launch_bounds__(kFvmThreads, 4)
   }
 }
 
+// Small grids (the paper's star experiments: 10^2..10^4 cells) are bound by
+// kernel launches, not work: one 1024-thread block runs every step, the two
+// phases separated by __syncthreads(), the stop test on a block reduction.
+// Same items, same per-cell operation sequence as the two-kernel path.
+constexpr int kSmallThreads = 1024;
+constexpr int64_t kSmallItems = 16384;  // rows + cells up to which one block runs the run
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    fvm_small_kernel(const __grid_constant__ gsde_fvm_desc d, double *rho, double *scratch,
+                     int64_t n_steps, double dt, double neg_floor, int64_t *neg_step,
+                     unsigned long long *red) {
+  __shared__ double s_amax[kSmallThreads / 32], s_nmin[kSmallThreads / 32];
+  const int64_t n_ser = d.n_vser > 0 ? 1 : 0;
+  const int tid = threadIdx.x;
+  int64_t done = 0;
+  for (int64_t step = 0; step < n_steps; ++step) {
+    const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+    double amax = 0.0, nmin = 0.0;
+    for (int64_t it = tid; it < d.n_pslot + d.n_cells; it += kSmallThreads) {
+      if (it < d.n_pslot) {
+        exchange_row(f, it);
+      } else {
+        const int64_t c = it - d.n_pslot;
+        if (!(d.cell_flags[c] & kOwned)) {
+          const double v = f.base(c);
+          f.out[c] = v;
+          track(v, amax, nmin);
+        }
+      }
+    }
+    __syncthreads();  // terms written
+    for (int64_t it = tid; it < n_ser + d.n_pslot; it += kSmallThreads) {
+      if (it < n_ser) {
+        for (int64_t k = 0; k < d.n_vser; ++k) f.init_cells(d.vser[k]);
+        for (int64_t k = 0; k < d.n_vser; ++k) f.vertex_global(d.vser[k]);
+        for (int64_t k = 0; k < d.n_vser; ++k)
+          for (int64_t i = d.v_off[d.vser[k]]; i < d.v_off[d.vser[k] + 1]; ++i)
+            track(f.out[d.v_cells[i]], amax, nmin);
+      } else {
+        const int64_t t = it - n_ser;
+        const int64_t c = d.v_cells[d.pslot[t]];
+        double val = f.base(c);
+        for (int64_t m = d.tstart[t]; m < d.tstart[t + 1]; ++m) val += d.terms[m];
+        f.out[c] = val;
+        track(val, amax, nmin);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      nmin = fmax(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
+    }
+    if ((tid & 31) == 0) {
+      s_amax[tid >> 5] = amax;
+      s_nmin[tid >> 5] = nmin;
+    }
+    __syncthreads();  // new densities and the warp maxima are in
+    amax = s_amax[0];
+    nmin = s_nmin[0];
+    for (int w = 1; w < kSmallThreads / 32; ++w) {
+      amax = fmax(amax, s_amax[w]);
+      nmin = fmax(nmin, s_nmin[w]);
+    }
+    __syncthreads();  // everyone read the maxima before the next step rewrites them
+    done = step + 1;
+    if (-nmin < neg_floor * fmax(1.0, amax)) {  // fvm.py:329-337
+      if (tid == 0) *neg_step = step + 1;
+      break;
+    }
+  }
+  if (done & 1)
+    for (int64_t c = tid; c < d.n_cells; c += kSmallThreads) rho[c] = scratch[c];
+  if (tid == 0) red[3] = (unsigned long long)done;
+}
+
 // after an odd number of completed steps the newest density is in scratch
 __global__ void fvm_finish_kernel(double *rho, const double *scratch, int64_t n_cells,
                                   const unsigned long long *red) {
@@ -304,6 +379,12 @@ cudaError_t launch_fvm(const gsde_fvm_desc &d, double *rho, double *scratch, int
   if (err == cudaSuccess) err = cudaMemsetAsync(neg_step, 0, sizeof(int64_t), s);
   if (err != cudaSuccess) return err;
   unsigned long long *r = reinterpret_cast<unsigned long long *>(red);
+  if (d.n_pslot + d.n_cells <= kSmallItems) {
+    fvm_small_kernel<<<1, kSmallThreads, 0, s>>>(d, rho, scratch, n_steps, dt, neg_floor,
+                                                  neg_step, r);
+    count_launch();
+    return cudaGetLastError();
+  }
   int device = 0;
   cudaGetDevice(&device);
   int per1 = 0, per2 = 0;

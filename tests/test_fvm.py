@@ -204,3 +204,28 @@ def test_term_layout_is_a_permutation(name):
         k = sl - lo
         want = (n - 1) * active[k] + (active.sum() - active[k]) + (n - 1)
         assert p.tstart[t + 1] - p.tstart[t] == want
+
+
+@pytest.mark.gpu
+def test_gpu_vs_oracle_multiblock_path():
+    """A grid above the single-block threshold (two kernels per step, CUDA-graph
+    replay, stop test in the last block): bit for bit against the oracle, and a
+    forced-unstable run stops at the oracle's step."""
+    from oracle import oracle
+
+    text = open(os.path.join(HERE, "golden", "vascular_small.graph")).read()
+    g, f = gs.parse_graph_file(text)
+    rng = np.random.default_rng(4)
+    grid = gs.EdgeGrid(counts=rng.integers(30, 60, g.n_edges), lengths=g.edge_length)
+    p = fvm._pack(g, f, grid)
+    assert p.pslot.size + grid.n_cells > 16384  # csrc/gsde_fvm.cu kSmallItems
+    dt = 0.9 * fvm.stability_limit(g, f, grid)
+    rho0 = rng.random(grid.n_cells)
+    ref, n_ref = oracle.fvm_steps(rho0, 150, dt, p.reference_tuple())
+    got, n = fvm.fvm_steps_device(g, f, grid, rho0, 150, dt)
+    assert n == n_ref == 0
+    assert np.array_equal(got, ref)
+    ref, n_ref = oracle.fvm_steps(rho0, 150, 4.0 * dt, p.reference_tuple())
+    got, n = fvm.fvm_steps_device(g, f, grid, rho0, 150, 4.0 * dt)
+    assert n_ref > 0 and n == n_ref
+    assert np.array_equal(got, ref)
