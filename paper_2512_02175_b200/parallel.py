@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-ESTIMATORS = ("m_hist", "totals", "edge_counts", "hist")
+ESTIMATORS = ("m_hist", "totals", "edge_counts", "hist", "exit_counts")
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -89,3 +89,27 @@ def run_ensemble_distributed(graph, field, config, grid=None, group=None,
         n_particles=config.n_particles,
         shard=(off, cnt),
     )
+
+
+def exit_counts_distributed(graph, field, dt, n_trials, seed, vertex=0, max_splits=100,
+                            rng="native", group=None):
+    """Vertex trials (the estimator behind ``exit_probability_experiment``,
+    reference ``analysis.py:348-384``) sharded by global trial id over the
+    ranks; exit counts, M histogram and totals merged with one all-reduce.
+    Identical to a 1-GPU :func:`analysis.vertex_exit_counts` for any world size."""
+    import torch.distributed as dist
+
+    from .analysis import ExitCounts
+    from .coefficients import gamma as vgamma
+    from .engine import trials_device
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    off, cnt = shard_range(n_trials, rank, world)
+    res = trials_device(graph, field, dt, cnt, seed, vertex, max_splits, rng, per_trial=False,
+                        trial_offset=off)
+    merged = merge_estimators(res, group)
+    tot = merged["totals"].cpu().numpy()
+    return ExitCounts(merged["exit_counts"].cpu().numpy(), merged["m_hist"].cpu().numpy(),
+                      int(n_trials), int(tot[0]), int(tot[1]), int(tot[2]),
+                      vgamma(field, graph, vertex, dt))

@@ -333,3 +333,22 @@ def test_native_invariants_random_graphs(seed):
     assert int(cr.sum()) == int(tot[0]) and int(ev.sum()) == int(tot[1])
     assert int(mh.sum()) == int(tot[1])
     assert int(d["truncs"].cpu().numpy().sum()) == int(tot[2])
+
+
+def test_exit_counts_sharded_equal_single_run():
+    """Trial sharding by global id (the multi-GPU C3 path): shards summed equal
+    one launch exactly, for both streams."""
+    from paper_2512_02175_b200 import parallel
+
+    g, f = workloads.star5("linear")
+    for rng_ in ("native", "reference"):
+        one = analysis.vertex_exit_counts(g, f, 1e-3, 300_001, 5, rng=rng_)
+        parts = [engine.trials_device(g, f, 1e-3, c, 5, rng=rng_, per_trial=False,
+                                      trial_offset=o)
+                 for o, c in (parallel.shard_range(300_001, r, 3) for r in range(3))]
+        np.testing.assert_array_equal(sum(p["exit_counts"] for p in parts).cpu().numpy(),
+                                      one.counts)
+        np.testing.assert_array_equal(sum(p["m_hist"] for p in parts).cpu().numpy(),
+                                      one.m_histogram)
+    ec = parallel.exit_counts_distributed(g, f, 1e-3, 300_001, 5)  # world 1
+    np.testing.assert_array_equal(ec.counts, analysis.vertex_exit_counts(g, f, 1e-3, 300_001, 5).counts)
