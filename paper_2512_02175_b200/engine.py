@@ -305,6 +305,7 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
 #: is the smallest, so little transfer is left exposed.
 _CHUNKS = (0.4, 0.3, 0.2, 0.1)
 _PIPELINE_MIN = 1 << 22
+_COPY_STREAMS: dict = {}  # device -> side stream for the device-to-host copies
 
 
 def _ensemble_to_host(graph, field, config):
@@ -321,7 +322,9 @@ def _ensemble_to_host(graph, field, config):
         return _to_host([res[k] for k in names + ("m_hist", "totals")])
     _, dev = _native.torch_cuda(config.device)
     compute = torch.cuda.current_stream(dev)
-    copier = torch.cuda.Stream(dev)
+    copier = _COPY_STREAMS.get(dev)
+    if copier is None:
+        copier = _COPY_STREAMS[dev] = torch.cuda.Stream(dev)
     hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
              for k in names]
     bounds = np.concatenate([[0], np.cumsum(np.floor(np.array(_CHUNKS) * n).astype(np.int64))])
