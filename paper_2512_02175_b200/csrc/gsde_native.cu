@@ -633,6 +633,8 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   Lane<C> L;
   L.x = 1.0f;
+  L.e = 0;  // idle lanes still evaluate the predicated per-trip code: keep indices valid
+  L.ev = make_int4(0, 0, 0, 0);
   L.len = star_len;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
   L.pend = false;
@@ -833,6 +835,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     if (active) start();
   };
   L.x = 1.0f;
+  L.e = 0;
+  L.ev = make_int4(0, 0, 0, 0);
   L.len = inf;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
   if (active) start();

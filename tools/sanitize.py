@@ -1,0 +1,36 @@
+"""Small runs of every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden"))
+import numpy as np
+import torch
+import cases
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import analysis, engine, fvm, workloads
+
+for case, init in (("star3_bm", gs.AtVertex(0)), ("hub8", gs.PerEdgeUniform(2.0)),
+                   ("random_general", gs.PerEdgeUniform(1.0)), ("star4_mixed", gs.AtVertex(0))):
+    g, f = cases.build(case, gs)
+    grid = gs.EdgeGrid.uniform(g, 4, lengths=None if not g.is_star else [2.0] * g.n_edges)
+    for rng in ("native", "reference"):
+        cfg = gs.SimulationConfig(dt=1e-3, n_steps=60, n_particles=3000, seed=1, rng=rng,
+                                  initial=init)
+        engine.ensemble_device(g, f, cfg, outputs=("all", "edge_counts"), grid=grid,
+                               occupation=(1, 5))
+    if g.is_star or not g.has_semi_infinite_edges:
+        for rng in ("native", "reference"):
+            engine.trials_device(g, f, 1e-3, 5000, 3, rng=rng)
+            engine.trials_device(g, f, 1e-3, 5000, 3, rng=rng, per_trial=False)
+g, f = workloads.vascular(3000, seed=2)
+grid = gs.EdgeGrid.uniform(g, 4)
+cfg = gs.SimulationConfig(dt=1e-3, n_steps=30, n_particles=20000, seed=2,
+                          initial=gs.PerEdgeUniform(float(g.edge_length.max())))
+engine.ensemble_device(g, f, cfg, outputs=("edge_counts",), grid=grid)
+gp, fp = cases.build("path3", gs)
+gridp = gs.EdgeGrid(counts=np.array([3, 1]), lengths=gp.edge_length)
+fvm.fvm_steps_device(gp, fp, gridp, np.linspace(1, 2, 4), 20, 0.5 * fvm.stability_limit(gp, fp, gridp))
+gridv = gs.EdgeGrid(counts=np.full(g.n_edges, 9), lengths=g.edge_length)
+fvm.fvm_steps_device(g, f, gridv, np.ones(gridv.n_cells), 3, 0.5 * fvm.stability_limit(g, f, gridv))
+analysis.histogram_accumulate(np.zeros(100, np.int64), np.linspace(0, 1, 100), gs.EdgeGrid.uniform(gp, 5))
+torch.cuda.synchronize()
+print("sanitize workload done")
