@@ -27,19 +27,24 @@ from paper_2512_02175_b200 import analysis, fvm, report, workloads
 out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
 os.makedirs(out, exist_ok=True)
 
+ONLY = os.environ.get("TABLES_ONLY", "")
+
 # 1. exit probabilities
 g, f = workloads.star5("linear")
+rep = None
 t0 = time.time()
-rep = analysis.exit_probability_experiment(g, f, [1e-2, 1e-3, 1e-4, 1e-5], 10_000_000_000, 11)
-report.write_exit_prob_csv(os.path.join(out, "exit_prob.csv"), rep)
-print(f"exit-probability sweep: {time.time() - t0:.1f} s")
-for r in rep.rows:
+if not ONLY or ONLY == "1":
+    rep = analysis.exit_probability_experiment(g, f, [1e-2, 1e-3, 1e-4, 1e-5], 10_000_000_000,
+                                               11)
+    report.write_exit_prob_csv(os.path.join(out, "exit_prob.csv"), rep)
+    print(f"exit-probability sweep: {time.time() - t0:.1f} s")
+for r in (rep.rows if rep else ()):
     print(f"  dt={r.dt:g} max|freq-b|={r.max_deviation:.3e} se={r.binomial_se.max():.1e} "
           f"mean M={r.mean_crossings:.3f}")
 
 # 2. EM vs FVM
 rows = []
-for kind in ("linear", "quadratic"):
+for kind in (("linear", "quadratic") if not ONLY or ONLY == "2" else ()):
     g, f = workloads.star5(kind)
     orc = analysis.SteadyStateOracle.from_field(g, f)
     lengths = orc.truncation_lengths(1e-8)
@@ -60,4 +65,28 @@ for kind in ("linear", "quadratic"):
                  dict(method=f"fvm_{kind}", dt=dt_f, cells_per_edge=cells, l2_error=fv)]
         print(f"{kind} cells={cells}: EM L2={em:.4f} ({t_em:.1f} s, 1e13 psteps, "
               f"truncations {st.truncation_count}); FVM L2={fv:.4f} ({n_f} steps, {t_fv:.1f} s)")
-report.write_error_table_csv(os.path.join(out, "error_table.csv"), rows)
+if rows:
+    report.write_error_table_csv(os.path.join(out, "error_table.csv"), rows)
+
+# 3. Crossing statistics vs Thm 3.1 / the chi-squared law (homogeneous star, 1e10 trials
+#    per stream): M histogram of vertex trials, fused on the device
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "tests", "golden"))
+import cases  # noqa: E402
+from paper_2512_02175_b200.engine import BounceStats  # noqa: E402
+
+g, f = cases.build("star_homog", gs)
+for rng, n in ((("native", 10_000_000_000), ("reference", 1_000_000_000))
+               if not ONLY or ONLY == "3" else ()):
+    t0 = time.time()
+    ec = analysis.vertex_exit_counts(g, f, 1e-3, n, 21, rng=rng)
+    bs = BounceStats(m_histogram=ec.m_histogram, gamma=ec.gamma,
+                     truncation_count=ec.truncation_count, crossings_total=ec.crossings_total,
+                     crossing_events=ec.crossing_events)
+    cb = analysis.check_crossing_bound(bs)
+    report.write_bounces_csv(os.path.join(out, f"bounces_{rng}.csv"), bs)
+    report.write_bound_check_csv(os.path.join(out, f"bound_check_{rng}.csv"), cb)
+    worst = max(abs(r.empirical - r.chi2_tail) / r.std_error for r in cb.rows)
+    print(f"crossing law ({rng}, {n:.0e} trials, {time.time() - t0:.1f} s): gamma={cb.gamma:.4f} "
+          f"bound violated={cb.any_bound_violation} chi2 deviates={cb.any_chi2_deviation} "
+          f"max |emp-chi2|/se={worst:.2f}")
