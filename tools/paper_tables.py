@@ -90,3 +90,40 @@ for rng, n in ((("native", 10_000_000_000), ("reference", 1_000_000_000))
     print(f"crossing law ({rng}, {n:.0e} trials, {time.time() - t0:.1f} s): gamma={cb.gamma:.4f} "
           f"bound violated={cb.any_bound_violation} chi2 deviates={cb.any_chi2_deviation} "
           f"max |emp-chi2|/se={worst:.2f}")
+
+# 4. Native vs reference stream at scale: snapshot densities (two-sample chi-square)
+from scipy import stats as _st  # noqa: E402
+
+
+def _chi2(h1, h2, min_count=20):
+    h1, h2 = np.asarray(h1, np.float64), np.asarray(h2, np.float64)
+    keep = (h1 + h2) >= min_count
+    a, b = h1[keep], h2[keep]
+    k1, k2 = np.sqrt(b.sum() / a.sum()), np.sqrt(a.sum() / b.sum())
+    chi2 = float((((k1 * a - k2 * b) ** 2) / (a + b)).sum())
+    dof = int(keep.sum()) - 1
+    return float(_st.chi2.sf(chi2, dof)), chi2, dof
+
+
+for name, build, init, steps, n_nat, n_ref, cells in (
+        ("C2 hub64", workloads.hub64, lambda g: gs.PerEdgeUniform(2.0), 1000,
+         1_000_000_000, 100_000_000, 8),
+        ("C4 vascular", workloads.vascular,
+         lambda g: gs.PerEdgeUniform(float(g.edge_length.max())), 100,
+         1_000_000_000, 100_000_000, 2)):
+    if ONLY and ONLY != "4":
+        break
+    g, f = build()
+    grid = gs.EdgeGrid.uniform(g, cells)
+    res = {}
+    for rng, n, seed in (("native", n_nat, 31), ("reference", n_ref, 32)):
+        t0 = time.time()
+        cfg = gs.SimulationConfig(dt=1e-3, n_steps=steps, n_particles=n, seed=seed,
+                                  initial=init(g), rng=rng)
+        h, st = analysis.run_ensemble_histogram(g, f, cfg, grid)
+        res[rng] = (h.counts, st.crossings_total / (n * steps), time.time() - t0)
+    p, chi2, dof = _chi2(res["native"][0], res["reference"][0])
+    print(f"{name}: native {n_nat:.0e} vs reference {n_ref:.0e} particles x {steps} steps: "
+          f"density chi2 p={p:.3g} (chi2={chi2:.0f}, dof={dof}); crossings/pstep "
+          f"{res['native'][1]:.6f} vs {res['reference'][1]:.6f}; "
+          f"{res['native'][2]:.1f} s / {res['reference'][2]:.1f} s")
