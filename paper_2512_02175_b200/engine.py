@@ -22,6 +22,7 @@ unchanged:
 
 from __future__ import annotations
 
+import dataclasses
 import math
 from dataclasses import dataclass, field as dataclass_field
 
@@ -106,6 +107,9 @@ class SimulationConfig:
     reflect_at: float = 0.0
     rng: str = "native"
     device: int | None = None
+    #: run_ensemble only: shard the particles (by global id) over these GPUs from
+    #: one process; results are identical to one device
+    devices: tuple | None = None
 
     def validated(self, graph: MetricGraph) -> "SimulationConfig":
         """Reference checks (``engine.py:114-139``) plus the ``rng`` mode."""
@@ -121,6 +125,9 @@ class SimulationConfig:
             raise ConfigInvalid("reflect_at must be nonnegative")
         if self.rng not in RNG_MODES:
             raise ConfigInvalid(f"rng must be one of {RNG_MODES}, got {self.rng!r}")
+        if self.devices is not None and (len(self.devices) < 1 or
+                                         any(int(d) < 0 for d in self.devices)):
+            raise ConfigInvalid("devices must be a non-empty sequence of device indices")
         init = self.initial
         if isinstance(init, AtVertex):
             if not (0 <= init.vertex < graph.n_vertices):
@@ -288,8 +295,14 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
         z = np.zeros(0, np.int64)
         stats = BounceStats(np.zeros(cap + 1, np.int64), run_gamma, 0, 0, 0)
         return EnsembleResult(z, np.zeros(0), z.copy(), z.copy(), stats, config)
-    edges, positions, crossings, events, m_hist, totals = _ensemble_to_host(graph, field,
+    if config.devices is not None and len(config.devices) > 1:
+        edges, positions, crossings, events, m_hist, totals = _multi_device(graph, field,
                                                                            config)
+    else:
+        if config.devices is not None:
+            config = dataclasses.replace(config, device=int(config.devices[0]))
+        edges, positions, crossings, events, m_hist, totals = _ensemble_to_host(graph, field,
+                                                                               config)
     stats = BounceStats(
         m_histogram=m_hist,
         gamma=run_gamma,
@@ -345,6 +358,40 @@ def _ensemble_to_host(graph, field, config):
     copier.synchronize()
     m_hist = sum(r["m_hist"] for r in parts).cpu().numpy()
     totals = sum(r["totals"] for r in parts).cpu().numpy()
+    return [h.numpy() for h in hosts] + [m_hist, totals]
+
+
+def _multi_device(graph, field, config):
+    """run_ensemble over several GPUs of this process: contiguous particle-id
+    shards (the streams are keyed by global id), one launch per device queued
+    on each device's current stream before any result is read, per-particle
+    arrays gathered into pinned host memory, integer estimators summed."""
+    import torch
+
+    from .parallel import shard_range
+
+    names = ("edge", "x", "crossings", "events")
+    n = config.n_particles
+    devs = [int(d) for d in config.devices]
+    hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
+             for k in names]
+    parts = []
+    for r, d in enumerate(devs):
+        off, cnt = shard_range(n, r, len(devs))
+        if cnt == 0:
+            continue
+        with torch.cuda.device(d):
+            res = ensemble_device(graph, field, dataclasses.replace(config, device=d),
+                                  pid_offset=off, n_particles=cnt, outputs=names)
+            for h, k in zip(hosts, names):
+                h[off:off + cnt].copy_(res[k], non_blocking=True)
+        parts.append((d, res))
+    m_hist = np.zeros(config.max_splits_per_step + 1, np.int64)
+    totals = np.zeros(4, np.int64)
+    for d, res in parts:
+        torch.cuda.current_stream(d).synchronize()
+        m_hist += res["m_hist"].cpu().numpy()
+        totals += res["totals"].cpu().numpy()
     return [h.numpy() for h in hosts] + [m_hist, totals]
 
 

@@ -9,6 +9,8 @@ and Thm 3.1 bound, the paper's steady-state L2 targets (SPEC acceptance 5, 6,
 11) and size-independent invariants at full benchmark sizes.
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -352,3 +354,20 @@ def test_exit_counts_sharded_equal_single_run():
                                       one.m_histogram)
     ec = parallel.exit_counts_distributed(g, f, 1e-3, 300_001, 5)  # world 1
     np.testing.assert_array_equal(ec.counts, analysis.vertex_exit_counts(g, f, 1e-3, 300_001, 5).counts)
+
+
+def test_devices_option_equals_single_device():
+    """SimulationConfig(devices=...) shards by global particle id over the listed
+    GPUs of one process (here cuda:0 twice): identical to one device."""
+    g, f = workloads.hub64()
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=50, n_particles=100_003, seed=4,
+                              initial=gs.PerEdgeUniform(2.0))
+    a = gs.run_ensemble(g, f, cfg)
+    b = gs.run_ensemble(g, f, dataclasses.replace(cfg, devices=(0, 0, 0)))
+    np.testing.assert_array_equal(a.edges, b.edges)
+    np.testing.assert_array_equal(a.positions, b.positions)
+    np.testing.assert_array_equal(a.crossings, b.crossings)
+    np.testing.assert_array_equal(a.stats.m_histogram, b.stats.m_histogram)
+    assert a.stats.crossings_total == b.stats.crossings_total
+    with pytest.raises(gs.ConfigInvalid):
+        gs.run_ensemble(g, f, dataclasses.replace(cfg, devices=()))
