@@ -382,14 +382,14 @@ struct Lane {
 // vertex (x == 0, possibly with an unresolved overshoot from an earlier trip)
 // or beyond the optional mirror wall.  Returns true when the macro step
 // completed.
-template <class C>
+template <class C, bool PEND>
 __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
                                           const Tables<C::SMEM> &T, const Occ &O,
                                           const NatParams &p, float z, uint32_t u) {
-  if (L.pend) {
+  if (PEND && L.x < 0.0f) {  // pending hit: the trip stored -px in x (x > 0 before a hit)
+    L.px = -L.x;
     L.dtr = fmaxf(L.split_factor(G) * L.dtr, 0.0f);
     L.sq = fast_sqrt(L.dtr);
-    L.pend = false;
   }
   // sample the exit edge, one-sided |W| excursion (kernels.py:198-220)
   L.M += 1;
@@ -463,12 +463,13 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
   return false;
 }
 
-template <class C>
+// PEND: the lane may carry an unresolved hit (ensembles; trials never do)
+template <class C, bool PEND = true>
 __device__ __forceinline__ bool rare_trip(Lane<C> &L, const NativeGraph &G,
                                           const Tables<C::SMEM> &T, const Occ &O,
                                           const NatParams &p, float z, uint32_t u) {
   if constexpr (C::STAR)
-    return rare_star<C>(L, G, T, O, p, z, u);
+    return rare_star<C, PEND>(L, G, T, O, p, z, u);
   else
     return rare_general<C>(L, G, T, O, p, z, u);
 }
@@ -479,8 +480,9 @@ __device__ __forceinline__ bool rare_trip(Lane<C> &L, const NativeGraph &G,
 // Common path: a lane strictly inside its edge always begins a fresh macro
 // step (dtr == dt), so the proposal uses cached constants.  Accepted: done
 // (the star mirror wall reflects in place, kernels.py:185-188).  Overshoot
-// at an end: the hit is recorded with predicated moves (x = the vertex, start
-// point and Gaussian saved) and its split time is solved by the lane's next
+// at an end: the hit is recorded with predicated moves (general: x = the
+// vertex, start point and Gaussian saved; star: x = -start point, Gaussian
+// saved) and its split time is solved by the lane's next
 // vertex trip, so all vertex work is one divergent region.  That region is
 // compiled only into the vertex-slot trip (SLOT), the first trip of every
 // Q-trip iteration; lanes at a vertex wait for it, so the warp resolves its
@@ -497,11 +499,15 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
   const bool hit = run && !ok;
   if (C::REFLECT && xn > L.len) xn = fmaxf(2.0f * L.len - xn, 0.0f);
   if (hit) {
-    if (!C::STAR) L.M += 1;  // general counts hits; star counts vertex iterations
-    L.pend = true;
-    L.px = L.x;
     L.pz = z;
-    L.x = (C::STAR || !lo_ok) ? 0.0f : L.len;
+    if (C::STAR) {  // star: the pending flag and start point live in x's sign
+      L.x = -L.x;
+    } else {        // general counts hits; star counts vertex iterations
+      L.M += 1;
+      L.pend = true;
+      L.px = L.x;
+      L.x = lo_ok ? L.len : 0.0f;
+    }
   }
   if (ok) L.x = xn;
   bool done = ok;
@@ -847,8 +853,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     float z0, z1;
     box_muller(r.x, r.y, z0, z1);
     bool fin = false;
-    if (active) fin = rare_trip<C>(L, G, T, O, p, z0, r.z);
-    if (active && !fin) fin = rare_trip<C>(L, G, T, O, p, z1, r.w);
+    if (active) fin = rare_trip<C, false>(L, G, T, O, p, z0, r.z);
+    if (active && !fin) fin = rare_trip<C, false>(L, G, T, O, p, z1, r.w);
     if (fin) finish();
   }
   if (o.totals) {
