@@ -183,7 +183,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   std::vector<uint64_t> thresh(S);
   std::vector<double> len64(E), coef64(E), sig64(E), tabx64(T ? T : 1), tabmu64(T ? T : 1);
   std::vector<float> len32(E), coef32(E), sig32(E), tabx32(T ? T : 1), tabmu32(T ? T : 1);
-  bool has_tab = false;
+  bool has_tab = false, zero_drift = true;
   for (int64_t e = 0; e < E; ++e) {
     einit[e] = (int32_t)d->edge_init[e];
     eterm[e] = (int32_t)d->edge_term[e];
@@ -195,6 +195,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     sig64[e] = d->sigma[e];
     sig32[e] = (float)d->sigma[e];
     if (kind[e] == 2) has_tab = true;
+    if (kind[e] == 2 || d->dcoef[e] != 0.0) zero_drift = false;
     if (kind[e] > 2) return set_error(GSDE_EINVAL, "graph_create: bad drift kind on edge %lld",
                                       (long long)e);
   }
@@ -224,7 +225,8 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     // length) also lies within the reference's FP64 edge [0, l]
     r.x = len32[e];
     if (std::isfinite(len64[e]) && (double)r.x > len64[e]) r.x = std::nextafter(r.x, 0.0f);
-    r.w = sig32[e];
+    // sigma * sqrt(2 ln 2): the native Box-Muller returns z / sqrt(2 ln 2)
+    r.w = (float)(d->sigma[e] * 1.1774100225154747);
     if (kind[e] == 0) {
       r.y = coef32[e];
       r.z = 0.0f;
@@ -318,6 +320,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   g->T = T;
   g->is_star = d->is_star != 0;
   g->has_tab = has_tab;
+  g->zero_drift = zero_drift;
   g->arena = dev;
   g->arena_bytes = (int64_t)arena_bytes;
   g->work = (unsigned long long *)P(o_work);

@@ -13,6 +13,7 @@ struct gsde_graph_s {
   int64_t E = 0, V = 0, S = 0, T = 0;
   bool is_star = false;
   bool has_tab = false;
+  bool zero_drift = false;  // every edge driftless (kind 0/1 with coefficient 0)
   void *arena = nullptr;
   int64_t arena_bytes = 0;
   gsde::RefGraph<double> ref64{};

@@ -82,11 +82,13 @@ __device__ __forceinline__ float fast_lg2(float v) {
 }
 
 // Box-Muller on two 32-bit words: u1 in (0, 1] with 2^-33 resolution near 0
-// (|z| <= 6.8), angle uniform on [-pi, pi).
+// (|z| <= 6.8), angle uniform on [-pi, pi).  Returns z / sqrt(2 ln 2): the
+// native edge records carry sigma * sqrt(2 ln 2) (gsde_abi.cu), so every
+// sigma * z product is unchanged and the scale costs no instruction here.
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = fmaf((float)a, 0x1p-32f, 0x1p-33f);
-  // u1 <= 1 so -2 ln u1 >= 0 (lg2.approx(1) == 0)
-  const float r = fast_sqrt(fast_lg2(u1) * -1.3862943611198906f);
+  // u1 <= 1 so -log2 u1 >= 0 (lg2.approx(1) == 0)
+  const float r = fast_sqrt(-fast_lg2(u1));
   float s, c;
   __sincosf((float)(int32_t)b * 1.4629180792671596e-9f, &s, &c);  // pi * 2^-31
   z0 = r * c;
@@ -169,13 +171,15 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 }
 
 // Compile-time kernel variant.
-template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_>
+template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
   static constexpr bool TAB = TAB_;          // some edge has a tabulated drift
   static constexpr bool REFLECT = REFLECT_;  // star mirror wall enabled
   static constexpr bool OCC = OCC_;          // time-integrated occupation histogram
+  static constexpr bool ZD = ZD_;            // Brownian: every drift is zero
+  static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
 };
 
 // Occupation histogram: grid arrays + counters (shared uint32 or global int64).
@@ -332,6 +336,7 @@ struct Lane {
   }
 
   __device__ __forceinline__ float drift(const NativeGraph &G, float at) const {
+    if (C::ZD) return 0.0f;
     if (C::TAB && isnan(mu_b)) return drift_tab(G, e, at);
     return fmaf(mu_b, at, mu_a);
   }
@@ -340,9 +345,15 @@ struct Lane {
   // left the edge through the vertex the lane now sits at (kernels.py:190-195,
   // :276-283); residual time (1 - s^2) dtr
   __device__ __forceinline__ float split_factor(const NativeGraph &G) const {
-    const float a = drift(G, px) * dtr;
     const float b = (sig * sq) * pz;
     const bool lo = C::STAR || !(x > 0.0f);
+    if (C::ZD) {  // split_root(0, bb, c): the linear root s = -c / bb, same fallbacks
+      const float c = lo ? px : len - px, bb = lo ? b : -b;
+      if (c == 0.0f) return bb <= 0.0f ? 1.0f : 0.0f;
+      const float s = c * fast_rcp(-bb);
+      return (s >= 0.0f && s <= 1.0f) ? 1.0f - s * s : 0.0f;
+    }
+    const float a = drift(G, px) * dtr;
     const float s = lo ? split_root(a, b, px) : split_root(-a, -b, len - px);
     return 1.0f - s * s;
   }
@@ -396,8 +407,8 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
   L.load_edge(T, O, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
   const float w = fabsf(z);
   const float mu0 = L.drift(G, 0.0f);
-  const float xn = fmaf(L.sig * L.sq, w, mu0 * L.dtr);
-  if (xn >= 0.0f) {
+  const float xn = C::ZD ? (L.sig * L.sq) * w : fmaf(L.sig * L.sq, w, mu0 * L.dtr);
+  if (C::ZD || xn >= 0.0f) {
     L.x = (C::REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
     return true;
   }
@@ -450,7 +461,7 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
   }
   L.x = s < 0 ? L.len : 0.0f;
   const float mu = L.drift(G, L.x);
-  const float xn = fmaf(L.sig * L.sq, z, fmaf(mu, L.dtr, L.x));
+  const float xn = fmaf(L.sig * L.sq, z, C::ZD ? L.x : fmaf(mu, L.dtr, L.x));
   if (xn > 0.0f && xn < L.len) {
     L.x = xn;
     return true;
@@ -491,7 +502,7 @@ template <class C, bool SLOT>
 __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
                                      const Tables<C::SMEM> &T, const Shared &S, const Occ &O,
                                      const NatParams &p, float z, uint32_t u) {
-  float xn = fmaf(L.sig_sqdt, z, fmaf(L.drift(G, L.x), p.dt, L.x));
+  float xn = fmaf(L.sig_sqdt, z, C::ZD ? L.x : fmaf(L.drift(G, L.x), p.dt, L.x));
   const bool live = L.steps_left > 0;
   const bool run = live && (L.x > 0.0f) && (C::STAR || L.x < L.len);
   const bool lo_ok = xn > 0.0f;
@@ -952,15 +963,19 @@ cudaError_t prepare(K kernel, size_t smem) {
 
 // Runtime flags -> compile-time kernel variant (Cfg).
 template <bool OCC, class F>
-cudaError_t dispatch(bool star, bool smem, bool tab, bool reflect, F &&f) {
+cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
     constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
+    auto drift = [&](auto rf) -> cudaError_t {
+      constexpr bool RF = decltype(rf)::value;
+      if (tab) return f(Cfg<ST, SM, true, RF, OCC>{});
+      return zd ? f(Cfg<ST, SM, false, RF, OCC, true>{}) : f(Cfg<ST, SM, false, RF, OCC>{});
+    };
     if constexpr (ST)
-      if (reflect)
-        return tab ? f(Cfg<ST, SM, true, true, OCC>{}) : f(Cfg<ST, SM, false, true, OCC>{});
-    return tab ? f(Cfg<ST, SM, true, false, OCC>{}) : f(Cfg<ST, SM, false, false, OCC>{});
+      if (reflect) return drift(T{});
+    return drift(N{});
   };
   if (star) return smem ? with(T{}, T{}) : with(T{}, N{});
   return smem ? with(N{}, T{}) : with(N{}, N{});
@@ -1016,8 +1031,9 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
                   (unsigned)(qoff + queues));
   };
-  return occ ? dispatch<true>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run)
-             : dispatch<false>(g->is_star, stage, g->has_tab, p.reflect > 0.0f, run);
+  return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run)
+             : dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
+                               run);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
@@ -1030,7 +1046,8 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   const size_t smem = smem_bytes(g, a.cap + 1, stage, priv, 0);
   const int d = g->device;
   const int64_t n = a.n_trials;
-  return dispatch<false>(g->is_star, stage, g->has_tab, false, [&](auto cfg) -> cudaError_t {
+  return dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, false,
+                         [&](auto cfg) -> cudaError_t {
     const bool out = o.M || o.edge || o.x || o.trunc;
     auto k = out ? native_trials_kernel<decltype(cfg), true>
                  : native_trials_kernel<decltype(cfg), false>;

@@ -154,6 +154,30 @@ def test_reflected_brownian_motion_uniform():
     assert err < 0.02, err
 
 
+@pytest.mark.parametrize("geom", ["star", "general"])
+def test_zero_drift_variant_matches_generic_kernel(geom):
+    """Driftless fields run a specialised kernel (no drift terms, linear split
+    root).  A drift of 1e-30 takes the generic kernel with the same streams and
+    - within FP32 rounding - the same dynamics: nearly every particle must end
+    on the same edge at the same position, with the same crossing counts."""
+    if geom == "star":
+        g = gs.build_graph([(0, None, float("inf"))] * 3)
+        init, steps = gs.AtVertex(0), 1000
+    else:
+        g, _ = workloads.hub64()
+        init, steps = gs.PerEdgeUniform(2.0), 300
+    E = g.n_edges
+    mk = lambda mu: gs.CoefficientField.for_graph(g, [gs.ConstantDrift(mu)] * E, [1.0] * E)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=steps, n_particles=200_000, seed=17, initial=init)
+    a = gs.run_ensemble(g, mk(0.0), cfg)
+    b = gs.run_ensemble(g, mk(1e-30), cfg)
+    same = (a.edges == b.edges) & (np.abs(a.positions - b.positions) <= 1e-4)
+    assert same.mean() > 0.999, same.mean()
+    assert np.mean(a.crossings == b.crossings) > 0.999
+    ca, cb = a.stats.crossings_total, b.stats.crossings_total
+    assert abs(ca - cb) <= 1e-3 * cb, (ca, cb)
+
+
 def test_native_determinism_and_sharding():
     g, f = workloads.hub64()
     cfg = gs.SimulationConfig(dt=1e-3, n_steps=100, n_particles=100_003, seed=21,
