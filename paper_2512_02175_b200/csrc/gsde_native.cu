@@ -298,8 +298,9 @@ struct Lane {
   float dtr, sq;   // time left in the current macro step and its sqrt
   int M;           // vertex resolutions in the current macro step
   bool trunc;
-  bool pend;       // a hit whose split time is not yet resolved:
-  float px, pz;    //   proposal start x and its Gaussian (a, b re-derived)
+  // a hit whose split time is not yet resolved (pending): star x = -start,
+  // general steps_left < 0 with x = start; its Gaussian pz (a, b re-derived)
+  float px, pz;
   float mu_a, mu_b, sig, sig_sqdt;  // cached drift / diffusion of e
   float len;       // edge length (star: mirror wall or +inf)
   int4 ev;         // endpoint alias info of e (general graphs)
@@ -431,9 +432,16 @@ template <class C>
 __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
                                              const Tables<C::SMEM> &T, const Occ &O,
                                              const NatParams &p, float z, uint32_t u) {
-  if (L.pend) {
+  if (L.steps_left < 0) {  // pending hit (flag: the step count's sign; x = its start)
+    L.steps_left = -L.steps_left;
+    L.px = L.x;
+    // the proposal that overshot, recomputed bit for bit (a hit on the common
+    // path had dtr == dt and sq == sqrt(dt)), tells which end it reached
+    const float xn =
+        fmaf(L.sig * L.sq, L.pz, C::ZD ? L.px : fmaf(L.drift(G, L.px), L.dtr, L.px));
+    L.x = xn <= 0.0f ? 0.0f : L.len;
+    L.M += 1;
     L.dtr = L.split_factor(G) * L.dtr;
-    L.pend = false;
     if (L.dtr <= 0.0f) return true;  // step ends at the vertex, on the old edge
     if (L.M >= p.cap) {
       L.trunc = true;
@@ -466,11 +474,8 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
     L.x = xn;
     return true;
   }
-  L.M += 1;
-  L.pend = true;
-  L.px = L.x;
-  L.pz = z;
-  L.x = xn <= 0.0f ? 0.0f : L.len;
+  L.pz = z;  // zero-time re-hit: pending from the vertex x
+  L.steps_left = -L.steps_left;
   return false;
 }
 
@@ -511,18 +516,14 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
   if (C::REFLECT && xn > L.len) xn = fmaxf(2.0f * L.len - xn, 0.0f);
   if (hit) {
     L.pz = z;
-    if (C::STAR) {  // star: the pending flag and start point live in x's sign
+    if (C::STAR)  // star: the pending flag and start point live in x's sign
       L.x = -L.x;
-    } else {        // general counts hits; star counts vertex iterations
-      L.M += 1;
-      L.pend = true;
-      L.px = L.x;
-      L.x = lo_ok ? L.len : 0.0f;
-    }
+    else  // general: the flag in the step count's sign, x stays the start
+      L.steps_left = -L.steps_left;
   }
   if (ok) L.x = xn;
   bool done = ok;
-  if (SLOT && live && !run) {
+  if (SLOT && (C::STAR ? live : L.steps_left != 0) && !run) {
     done = rare_trip<C>(L, G, T, O, p, z, u);
     if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
   }
@@ -560,7 +561,6 @@ __device__ __forceinline__ void start_particle(Lane<C> &L, const Tables<C::SMEM>
   L.sq = p.sqdt;
   L.M = 0;
   L.trunc = false;
-  L.pend = false;
   L.steps_left = p.n_steps;
   L.cross = L.events = L.truncs = 0;
   L.occ_left = O.start + O.every;
@@ -654,7 +654,6 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   L.ev = make_int4(0, 0, 0, 0);
   L.len = star_len;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
-  L.pend = false;
   L.M = 0;
   L.steps_left = 0;  // no particle in flight: every trip is a no-op
   L.occ_left = 1 << 30;
@@ -829,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     L.sq = p.sqdt;
     L.M = 0;
     L.trunc = false;
-    L.pend = false;
+    L.steps_left = 1;  // (general: the sign carries a pending re-hit)
     pair = 0;
   };
   auto finish = [&]() {
