@@ -154,7 +154,7 @@ def test_reflected_brownian_motion_uniform():
     assert err < 0.02, err
 
 
-@pytest.mark.parametrize("geom", ["star", "general"])
+@pytest.mark.parametrize("geom", ["star", "general", "general_l2"])
 def test_zero_drift_variant_matches_generic_kernel(geom):
     """Driftless fields run a specialised kernel (no drift terms, linear split
     root).  A drift of 1e-30 takes the generic kernel with the same streams and
@@ -163,9 +163,12 @@ def test_zero_drift_variant_matches_generic_kernel(geom):
     if geom == "star":
         g = gs.build_graph([(0, None, float("inf"))] * 3)
         init, steps = gs.AtVertex(0), 1000
-    else:
+    elif geom == "general":
         g, _ = workloads.hub64()
         init, steps = gs.PerEdgeUniform(2.0), 300
+    else:  # 2000-node network: tables read through L2, not staged in shared memory
+        g, _ = workloads.vascular(2000, seed=7)
+        init, steps = gs.PerEdgeUniform(float(g.edge_length.max())), 300
     E = g.n_edges
     mk = lambda mu: gs.CoefficientField.for_graph(g, [gs.ConstantDrift(mu)] * E, [1.0] * E)
     cfg = gs.SimulationConfig(dt=1e-3, n_steps=steps, n_particles=200_000, seed=17, initial=init)
