@@ -34,11 +34,18 @@ enum : uint8_t { kLeft = 1, kRight = 2, kOwned = 4 };
 
 // red[] layout: [0] max |rho|, [1] max(-rho) of the running step (double bit
 // patterns), [2] blocks finished, [3] steps done
-struct Fvm {
+// NC: the density read by a step is read-only for the whole kernel (the
+// one-step phase kernels), so it may take the non-coherent path (__ldg).  The
+// single-block kernel runs many steps in one launch and rewrites both buffers:
+// it reads the density with plain loads.
+template <bool NC>
+struct FvmT {
   const gsde_fvm_desc &d;
   double dt;
   const double *rho;
   double *out;
+
+  __device__ __forceinline__ double rd(int64_t c) const { return NC ? __ldg(rho + c) : rho[c]; }
 
   // interior face flux with drift mu between cells l and r (fvm.py:287-292)
   __device__ __forceinline__ double face(double mu, double D, double dx, double rl,
@@ -57,9 +64,9 @@ struct Fvm {
   __device__ __forceinline__ double base(int64_t c) const {
     const uint8_t fl = __ldg(d.cell_flags + c);
     const double D = __ldg(d.cell_D + c), dx = __ldg(d.cell_dx + c);
-    const double rc = __ldg(rho + c);
-    const double rl = (fl & kLeft) ? __ldg(rho + c - 1) : 0.0;
-    const double rr = (fl & kRight) ? __ldg(rho + c + 1) : 0.0;
+    const double rc = rd(c);
+    const double rl = (fl & kLeft) ? rd(c - 1) : 0.0;
+    const double rr = (fl & kRight) ? rd(c + 1) : 0.0;
     const double scale = dt / dx;
     double v = rc;
     if (fl & kLeft) v += scale * face(__ldg(d.cell_mu_l + c), D, dx, rl, rc);
@@ -130,6 +137,7 @@ __device__ __forceinline__ void track(double v, double &amax, double &nmin) {
 // exports i -> j and the diffusion pairs (i, j > i) -- written as signed terms
 // to the positions the destinations read them from (fvm._term_layout).  Every
 // term is the reference's own expression; a subtraction is stored negated.
+template <class Fvm>
 __device__ void exchange_row(const Fvm &f, int64_t t) {
   // every input is read-only during the step: __ldg lets the loads of later
   // iterations run ahead of this row's term stores
@@ -142,7 +150,7 @@ __device__ void exchange_row(const Fvm &f, int64_t t) {
   const int64_t *cell = d.v_cells + lo;
   const int64_t *pos = d.rpos + __ldg(d.rstart + t);
   const double dt = f.dt, bi = __ldg(b + i), dxi = __ldg(dx + i), Di = __ldg(Dd + i);
-  const double rho_i = __ldg(f.rho + __ldg(cell + i));
+  const double rho_i = f.rd(__ldg(cell + i));
   const double sp = __ldg(d.v_speed_in + sl), others = 1.0 - bi;
   if (sp > 0.0 && others > 0.0) {
     const double total = sp * rho_i;
@@ -159,7 +167,7 @@ __device__ void exchange_row(const Fvm &f, int64_t t) {
 #pragma unroll 2
   for (int j = i + 1; j < n; ++j) {
     const double bj = __ldg(b + j), dxj = __ldg(dx + j);
-    const double rj = __ldg(f.rho + __ldg(cell + j));
+    const double rj = f.rd(__ldg(cell + j));
     const int64_t p0 = __ldg(pos), p1 = __ldg(pos + 1);
     const double dpair = 0.5 * (Di + __ldg(Dd + j));
     const double dxh = 2.0 * dxi * dxj / (dxi + dxj);
@@ -225,7 +233,7 @@ __global__ void __launch_bounds__(kFvmThreads, 4)
                       double dt, const int64_t *neg_step, unsigned long long *red) {
   if (*(volatile const int64_t *)neg_step) return;  // an earlier step went negative
   const int64_t step = (int64_t)red[3];
-  const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+  const FvmT<true> f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
   const int64_t n_items = d.n_pslot + d.n_cells;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   double amax = 0.0, nmin = 0.0;  // max |rho|, max(-rho) over the cells written here
@@ -252,7 +260,7 @@ __global__ void __launch_bounds__(kFvmThreads, 4)
                       unsigned long long *red) {
   if (*(volatile int64_t *)neg_step) return;
   const int64_t step = (int64_t)red[3];
-  const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+  const FvmT<true> f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
   const int64_t n_ser = d.n_vser > 0 ? 1 : 0;
   const int64_t n_items = n_ser + d.n_pslot;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   const int tid = threadIdx.x;
   int64_t done = 0;
   for (int64_t step = 0; step < n_steps; ++step) {
-    const Fvm f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
+    const FvmT<false> f{d, dt, (step & 1) ? scratch : rho, (step & 1) ? rho : scratch};
     double amax = 0.0, nmin = 0.0;
     for (int64_t it = tid; it < d.n_pslot + d.n_cells; it += kSmallThreads) {
       if (it < d.n_pslot) {
