@@ -44,7 +44,12 @@ enum {
  *             machine in 14-proposal iterations.
  *             Statistically equivalent, not bit-identical, to REFERENCE. */
 enum { GSDE_STREAM_NATIVE = 0, GSDE_STREAM_REFERENCE = 1, GSDE_STREAM_INJECT = 2 };
-enum { GSDE_PREC_F32 = 0, GSDE_PREC_F64 = 1 };
+/* INJECT precisions: F32 / F64 run the reference-order stepper (gsde_ref.cu)
+ * in that precision; NATIVE runs the production FP32 kernel itself (the
+ * NATIVE stream's kernel with each proposal's normal and each exit uniform
+ * taken from the injected rows in the reference's order, exit slots by the
+ * reference's inverse CDF): ensembles only, no tabulated drift, no occ. */
+enum { GSDE_PREC_F32 = 0, GSDE_PREC_F64 = 1, GSDE_PREC_NATIVE = 2 };
 
 /* Initial placement codes (kernels.py:48-50). */
 enum { GSDE_INIT_POINT = 0, GSDE_INIT_PER_EDGE_UNIFORM = 1 };

@@ -24,6 +24,7 @@ GSDE_STREAM_REFERENCE = 1
 GSDE_STREAM_INJECT = 2
 GSDE_PREC_F32 = 0
 GSDE_PREC_F64 = 1
+GSDE_PREC_NATIVE = 2  # INJECT into the production FP32 kernel (ensembles)
 GSDE_INIT_POINT = 0
 GSDE_INIT_PER_EDGE_UNIFORM = 1
 

@@ -381,7 +381,8 @@ static int check_stream_args(int32_t stream, int32_t precision, const uint64_t *
   if (stream == GSDE_STREAM_INJECT) {
     if (!inj_raw || !inj_normal || inj_stride < 1)
       return set_error(GSDE_EINVAL, "%s: INJECT needs inj_raw, inj_normal and inj_stride", who);
-    if (precision != GSDE_PREC_F32 && precision != GSDE_PREC_F64)
+    if (precision != GSDE_PREC_F32 && precision != GSDE_PREC_F64 &&
+        precision != GSDE_PREC_NATIVE)
       return set_error(GSDE_EINVAL, "%s: unknown precision %d", who, precision);
   }
   return GSDE_OK;
@@ -411,11 +412,18 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
   if (rc) return rc;
   if (a->stream == GSDE_STREAM_NATIVE && a->n_steps > 0x7fffffffll)
     return set_error(GSDE_EINVAL, "ensemble: NATIVE stream supports n_steps < 2^31");
+  const bool native_inj = a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE;
+  if (native_inj && (g->has_tab || o->occ))
+    return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE supports neither tabulated drifts "
+                                  "nor the occupation histogram");
+  if (native_inj && (a->n_steps > 0x7fffffffll || a->inj_stride > 0x7fffffffll))
+    return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE needs n_steps, inj_stride < 2^31");
   if (a->n_particles == 0) return GSDE_OK;
   DeviceGuard guard(g->device);
   const cudaStream_t s = (cudaStream_t)stream;
-  const cudaError_t err = a->stream == GSDE_STREAM_NATIVE ? launch_native_ensemble(g, *a, *o, s)
-                                                          : launch_ref_ensemble(g, *a, *o, s);
+  const cudaError_t err = (a->stream == GSDE_STREAM_NATIVE || native_inj)
+                              ? launch_native_ensemble(g, *a, *o, s)
+                              : launch_ref_ensemble(g, *a, *o, s);
   return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "ensemble launch");
 }
 
@@ -430,6 +438,8 @@ int gsde_vertex_trials(const gsde_graph *g, const gsde_trials *a, const gsde_tri
   int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
                              "vertex_trials");
   if (rc) return rc;
+  if (a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE)
+    return set_error(GSDE_EINVAL, "%s: INJECT/NATIVE is an ensemble mode", "vertex_trials");
   if (a->n_trials == 0) return GSDE_OK;
   DeviceGuard guard(g->device);
   const cudaStream_t s = (cudaStream_t)stream;
@@ -450,6 +460,8 @@ int gsde_step_batch(const gsde_graph *g, const gsde_step_args *a, int64_t *edge,
   int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
                              "step_batch");
   if (rc) return rc;
+  if (a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE)
+    return set_error(GSDE_EINVAL, "%s: INJECT/NATIVE is an ensemble mode", "step_batch");
   DeviceGuard guard(g->device);
   const cudaError_t err = launch_step_batch(g, *a, edge, x, k, M, trunc, (cudaStream_t)stream);
   return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "step_batch launch");

@@ -69,6 +69,18 @@ struct NatParams {
   float start_x;
 };
 
+// Injected reference draws (Cfg::INJ ensembles): per particle [stride] raw
+// words and their normals, consumed in the reference's order (kernels.py:55-64)
+struct InjParams {
+  const uint64_t *raw;
+  const double *normal;
+  int64_t stride;
+  // the reference's slot tables in CSR order (exit slots by inverse CDF)
+  const uint64_t *thresh;
+  const int32_t *vedges;
+  const uint8_t *vorient;
+};
+
 __device__ __forceinline__ float fast_sqrt(float v) {
   float r;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
@@ -159,6 +171,17 @@ __device__ __forceinline__ int alias_pick(const Tables<SMEM> &T, int off, int de
   return lo < (uint32_t)c.x ? c.y : c.z;
 }
 
+// Injected-draw parity mode: the reference's exit slot for a raw draw -- the
+// first slot j of [off, off + deg) with (r >> 11) <= thresh[j], else the last
+// (kernels.py:134-143) -- as edge | orient << 31 like an alias pick.
+template <class L_>
+__device__ __forceinline__ int ref_pick(const L_ &L, int off, int deg, uint64_t raw) {
+  const uint64_t u53 = raw >> 11;
+  int j = off;
+  while (j < off + deg - 1 && u53 > __ldg(L.thr + j)) ++j;
+  return __ldg(L.ved + j) | ((int)__ldg(L.vor + j) << 31);
+}
+
 __device__ float drift_tab(const NativeGraph &G, int e, float x) {
   const int lo = G.tab_off[e], hi = G.tab_off[e + 1];
   if (x <= G.tab_x[lo]) return G.tab_mu[lo];
@@ -171,7 +194,8 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 }
 
 // Compile-time kernel variant.
-template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false>
+template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false,
+          bool INJ_ = false>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
@@ -179,6 +203,9 @@ struct Cfg {
   static constexpr bool REFLECT = REFLECT_;  // star mirror wall enabled
   static constexpr bool OCC = OCC_;          // time-integrated occupation histogram
   static constexpr bool ZD = ZD_;            // Brownian: every drift is zero
+  // parity mode: the production kernel fed the reference's injected draws
+  // (one per use, in the reference's order) and its inverse-CDF exit slots
+  static constexpr bool INJ = INJ_;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
 };
 
@@ -307,6 +334,27 @@ struct Lane {
   int steps_left;
   int cross, events, truncs;
   int occ_left;    // steps to the next occupation sample
+  // Cfg::INJ only: the reference's slot tables, this particle's injected
+  // draws and the next draw index
+  const uint64_t *thr;
+  const int32_t *ved;
+  const uint8_t *vor;
+  const uint64_t *ir;
+  const double *inn;
+  int k, kmax;
+  bool over;       // ran past the injected draws
+
+  // next injected normal, scaled like box_muller's output (z / sqrt(2 ln 2))
+  __device__ __forceinline__ float inj_gauss() {
+    if (k < kmax) return (float)(__ldg(inn + k++) * 0.84932180028801907);
+    over = true;
+    return 0.0f;
+  }
+  __device__ __forceinline__ uint64_t inj_raw() {
+    if (k < kmax) return __ldg(ir + k++);
+    over = true;
+    return 0ull;
+  }
 
   __device__ __forceinline__ void load_edge(const Tables<C::SMEM> &T, const Occ &O, int e2,
                                             float sqdt, float star_len) {
@@ -405,7 +453,12 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
   }
   // sample the exit edge, one-sided |W| excursion (kernels.py:198-220)
   L.M += 1;
-  L.load_edge(T, O, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
+  if constexpr (C::INJ) {  // the reference's order: the uniform, then the normal
+    L.load_edge(T, O, ref_pick(L, 0, G.n_edges, L.inj_raw()) & 0x7fffffff, p.sqdt, L.len);
+    z = L.inj_gauss();
+  } else {
+    L.load_edge(T, O, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
+  }
   const float w = fabsf(z);
   const float mu0 = L.drift(G, 0.0f);
   const float xn = C::ZD ? (L.sig * L.sq) * w : fmaf(L.sig * L.sq, w, mu0 * L.dtr);
@@ -452,7 +505,11 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
   const bool at_init = !(L.x > 0.0f);
   const int off = at_init ? L.ev.x : L.ev.z, deg = at_init ? L.ev.y : L.ev.w;
   int s;
-  if constexpr (C::SMEM) {
+  if constexpr (C::INJ) {  // the reference's order: the uniform, then the normal
+    s = ref_pick(L, off, deg, L.inj_raw());
+    L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
+    z = L.inj_gauss();
+  } else if constexpr (C::SMEM) {
     s = alias_pick(T, off, deg, u);
     L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
   } else {  // one round trip: column + both candidates' records in flight together
@@ -507,6 +564,8 @@ template <class C, bool SLOT>
 __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
                                      const Tables<C::SMEM> &T, const Shared &S, const Occ &O,
                                      const NatParams &p, float z, uint32_t u) {
+  if constexpr (C::INJ)  // one injected normal per proposal
+    z = (L.steps_left > 0 && L.x > 0.0f && (C::STAR || L.x < L.len)) ? L.inj_gauss() : 0.0f;
   float xn = fmaf(L.sig_sqdt, z, C::ZD ? L.x : fmaf(L.drift(G, L.x), p.dt, L.x));
   const bool live = L.steps_left > 0;
   const bool run = live && (L.x > 0.0f) && (C::STAR || L.x < L.len);
@@ -534,20 +593,35 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
 
 // Initial state of particle id (kernels.py:291-307, engine.py:194-203): the
 // edge and position only.
+// PerEdgeUniform from two raw 64-bit draws (kernels.py:298-305)
 template <bool SMEM>
-__device__ __forceinline__ void place_values(const NativeGraph &G, const Tables<SMEM> &T,
-                                             const NatParams &p, uint64_t id, int &e, float &x) {
+__device__ __forceinline__ void place_from_raw(const NativeGraph &G, const Tables<SMEM> &T,
+                                               const NatParams &p, uint64_t r0, uint64_t r1,
+                                               int &e, float &x) {
+  const double u = (double)(r0 >> 11) * kInv2p53;
+  const double u2 = (double)(r1 >> 11) * kInv2p53;
+  e = (int)(u * (double)G.n_edges);
+  if (e >= G.n_edges) e = G.n_edges - 1;
+  const double le = (double)T.E(e).x;
+  x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
+}
+
+// Particle i of this call: native placement stream, or (Cfg::INJ) the
+// reference's draws 0 and 1 of the particle's injected row.
+template <class C>
+__device__ __forceinline__ void place_values(const NativeGraph &G, const Tables<C::SMEM> &T,
+                                             const NatParams &p, const InjParams &q, int64_t i,
+                                             int &e, float &x) {
   if (p.init_kind == GSDE_INIT_POINT) {
     e = p.init_edge;
     x = fminf(p.init_x, T.E(e).x);  // the FP32 edge, like every native position
+  } else if constexpr (C::INJ) {
+    const uint64_t *r = q.raw + i * q.stride;
+    place_from_raw<C::SMEM>(G, T, p, __ldg(r), __ldg(r + 1), e, x);
   } else {
-    const Block r = native_block(p, 0u, kDomainPlace, id);
-    const double u = (double)((((uint64_t)r.x << 32) | r.y) >> 11) * kInv2p53;
-    const double u2 = (double)((((uint64_t)r.z << 32) | r.w) >> 11) * kInv2p53;
-    e = (int)(u * (double)G.n_edges);
-    if (e >= G.n_edges) e = G.n_edges - 1;
-    const double le = (double)T.E(e).x;
-    x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
+    const Block r = native_block(p, 0u, kDomainPlace, (uint64_t)(p.id_offset + i));
+    place_from_raw<C::SMEM>(G, T, p, ((uint64_t)r.x << 32) | r.y, ((uint64_t)r.z << 32) | r.w,
+                            e, x);
   }
 }
 
@@ -569,10 +643,11 @@ __device__ __forceinline__ void start_particle(Lane<C> &L, const Tables<C::SMEM>
 template <class C>
 __device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
                                              const Tables<C::SMEM> &T, const Occ &O,
-                                             const NatParams &p, uint64_t id, float star_len) {
+                                             const NatParams &p, const InjParams &q, uint64_t id,
+                                             float star_len) {
   int e;
   float x;
-  place_values<C::SMEM>(G, T, p, id, e, x);
+  place_values<C>(G, T, p, q, (int64_t)(id - (uint64_t)p.id_offset), e, x);
   start_particle<C>(L, T, O, p, e, x, star_len);
 }
 
@@ -626,7 +701,7 @@ template <class C, int Q, int SLOTS>
 __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
                            unsigned long long *work, unsigned queue_off,
-                           unsigned occ_tab_off) {
+                           unsigned occ_tab_off, InjParams q) {
   using IW = IterWords<Q, SLOTS>;
   constexpr int NB = IW::NB;
   const int nb = p.cap + 1;
@@ -659,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   L.occ_left = 1 << 30;
   uint32_t blk = 0;
   uint64_t id = 0;
-  int64_t t_cross = 0, t_events = 0, t_truncs = 0;
+  int64_t t_cross = 0, t_events = 0, t_truncs = 0, t_over = 0;
   bool waiting = i < p.n;  // next particle not started yet
   bool active = false;     // a particle is in flight
   bool need = false;       // finished: fetch the next particle id
@@ -669,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     t_cross += L.cross;
     t_events += L.events;
     t_truncs += L.truncs;
+    if (C::INJ) t_over += L.over ? 1 : 0;
     epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     queued = true;
     active = false;
@@ -677,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   if (p.n_steps == 0) {  // placement only (engine.py:329-336)
     while (waiting) {
       id = (uint64_t)(p.id_offset + i);
-      place_native(L, G, T, O, p, id, star_len);
+      place_native(L, G, T, O, p, q, id, star_len);
       epilogue_particle(o, i, L.e, (double)L.x, 0, 0, 0);
       epilogue_bins(o, L.e, (double)L.x);
       i += stride;
@@ -740,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
         const int64_t pi = (int64_t)base + lane;
         int e = 0;
         float x = 0.0f;
-        if (pi < p.n) place_values<C::SMEM>(G, T, p, (uint64_t)(p.id_offset + pi), e, x);
+        if (pi < p.n) place_values<C>(G, T, p, q, pi, e, x);
         const int slot = (int)((q_tail + lane) & (kRing - 1));
         WQ.pid[slot] = pi;
         WQ.pe[slot] = e;
@@ -755,6 +831,16 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
         if (waiting) {
           id = (uint64_t)(p.id_offset + i);
           start_particle<C>(L, T, O, p, WQ.pe[slot], WQ.px[slot], star_len);
+          if constexpr (C::INJ) {
+            L.thr = q.thresh;
+            L.ved = q.vedges;
+            L.vor = q.vorient;
+            L.ir = q.raw + i * q.stride;
+            L.inn = q.normal + i * q.stride;
+            L.k = p.init_kind == GSDE_INIT_POINT ? 0 : 2;  // placement used draws 0, 1
+            L.kmax = (int)q.stride;
+            L.over = false;
+          }
           blk = 0;
           waiting = false;
           active = true;
@@ -776,11 +862,15 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
 #pragma unroll
     for (int j = 0; j < Q; j += 2) {
       const unsigned fresh = IW::need(j) & ~(j ? IW::need(j - 2) : 0u);
+      float z0 = 0.0f, z1 = 0.0f;
+      if constexpr (!C::INJ) {  // (injected draws are taken per use inside the trips)
 #pragma unroll
-      for (int kb = 0; kb < NB; ++kb)
-        if (fresh & (1u << kb)) fill(kb);
-      float z0, z1;
-      box_muller(W[1 + j], W[2 + j], z0, z1);
+        for (int kb = 0; kb < NB; ++kb)
+          if (fresh & (1u << kb)) fill(kb);
+        box_muller(W[1 + j], W[2 + j], z0, z1);
+      } else {
+        for (int kb = 0; kb < 4 * NB; ++kb) W[kb] = 0u;
+      }
       if (IW::is_slot(j))
         trip<C, true>(L, G, T, S, O, p, z0, W[IW::uword(j)]);
       else
@@ -798,6 +888,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     warp_add_i64(&o.totals[0], t_cross);
     warp_add_i64(&o.totals[1], t_events);
     warp_add_i64(&o.totals[2], t_truncs);
+    if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
   shared_flush(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
 }
@@ -962,13 +1053,22 @@ cudaError_t prepare(K kernel, size_t smem) {
 
 // Runtime flags -> compile-time kernel variant (Cfg).
 template <bool OCC, class F>
-cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f) {
+cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
+                     bool inj = false) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
     constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
     auto drift = [&](auto rf) -> cudaError_t {
       constexpr bool RF = decltype(rf)::value;
+      if (inj) {  // parity mode: no tabulated drift, no occupation sampling
+        if constexpr (!OCC) {
+          if (tab) return cudaErrorInvalidValue;
+          return zd ? f(Cfg<ST, SM, false, RF, false, true, true>{})
+                    : f(Cfg<ST, SM, false, RF, false, false, true>{});
+        }
+        return cudaErrorInvalidValue;
+      }
       if (tab) return f(Cfg<ST, SM, true, RF, OCC>{});
       return zd ? f(Cfg<ST, SM, false, RF, OCC, true>{}) : f(Cfg<ST, SM, false, RF, OCC>{});
     };
@@ -991,6 +1091,9 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   p.init_edge = (int32_t)a.init_edge;
   p.init_x = (float)a.init_x;
   p.init_xmax = a.init_xmax;
+  const bool inj = a.stream == GSDE_STREAM_INJECT;  // (precision GSDE_PREC_NATIVE)
+  const InjParams q{a.inj_raw,        a.inj_normal,       a.inj_stride,
+                    g->ref32.v_thresh, g->ref32.v_edges, g->ref32.v_orient};
   const bool stage = g->nat_graph_smem > 0;
   const bool occ = o.occ != nullptr;
   const int d = g->device;
@@ -1028,11 +1131,12 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     err = cudaMemsetAsync(work, 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
     return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
-                  (unsigned)(qoff + queues));
+                  (unsigned)(qoff + queues), q);
   };
-  return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run)
+  return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
+                              inj)
              : dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                               run);
+                               run, inj);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,

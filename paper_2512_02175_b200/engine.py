@@ -211,7 +211,9 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
     (an :class:`EdgeGrid`) is given.  ``pid_offset`` / ``n_particles`` select
     a shard of global particle ids (multi-GPU).  ``inject=(raw, normal)``
     (device uint64 / float64 tensors ``[n, K]``) selects the injected-draw
-    stream with ``precision`` ``"f32"`` or ``"f64"``.  ``occupation=(every,
+    stream with ``precision`` ``"f32"`` or ``"f64"`` (the reference-order
+    stepper in that precision) or ``"native"`` (the production FP32 kernel
+    itself, fed one injected draw per use).  ``occupation=(every,
     start)`` (needs ``grid``) adds the time-integrated occupation histogram
     ``res["occ"]``: every particle's (edge, x) binned after every
     ``every``-th completed macro step beyond step ``start``.
@@ -273,7 +275,8 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
     if inject is not None:
         raw, nrm = inject
         r.stream = _native.GSDE_STREAM_INJECT
-        r.precision = _native.GSDE_PREC_F64 if precision == "f64" else _native.GSDE_PREC_F32
+        r.precision = {"f64": _native.GSDE_PREC_F64, "f32": _native.GSDE_PREC_F32,
+                       "native": _native.GSDE_PREC_NATIVE}[precision]
         r.inj_raw, r.inj_normal, r.inj_stride = raw.data_ptr(), nrm.data_ptr(), raw.shape[1]
     s = stream if stream is not None else _native.cur_stream(dev)
     _native.check(_native.lib().gsde_ensemble(dg.handle, r, o, s))
