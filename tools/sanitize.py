@@ -26,6 +26,15 @@ grid = gs.EdgeGrid.uniform(g, 4)
 cfg = gs.SimulationConfig(dt=1e-3, n_steps=30, n_particles=20000, seed=2,
                           initial=gs.PerEdgeUniform(float(g.edge_length.max())))
 engine.ensemble_device(g, f, cfg, outputs=("edge_counts",), grid=grid)
+# the production kernel under injected reference draws (INJECT/NATIVE), star + L2 graph
+rs = np.random.default_rng(3)  # any draws will do for memory checking
+for gg, ff, init, n in ((*cases.build("star3_bm", gs), gs.AtVertex(0), 2000),
+                        (g, f, gs.PerEdgeUniform(float(g.edge_length.max())), 2000)):
+    raw = rs.integers(0, 2**63, size=(n, 200), dtype=np.int64).view(np.uint64)
+    nrm = rs.standard_normal((n, 200))
+    inj = (torch.as_tensor(raw.view(np.int64)).cuda(), torch.as_tensor(nrm).cuda())
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=60, n_particles=n, seed=3, initial=init)
+    engine.ensemble_device(gg, ff, cfg, inject=inj, precision="native")
 gp, fp = cases.build("path3", gs)
 gridp = gs.EdgeGrid(counts=np.array([3, 1]), lengths=gp.edge_length)
 fvm.fvm_steps_device(gp, fp, gridp, np.linspace(1, 2, 4), 20, 0.5 * fvm.stability_limit(gp, fp, gridp))
