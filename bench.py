@@ -573,27 +573,37 @@ def main():
     kern_rate = wl.units_per_step * args.steps / kern  # per GPU, kernel only
     achieved = kern_rate * w_ops
 
+    # e2e through the public API with host buffers (graph upload + D2H): every
+    # rank runs its per-GPU share concurrently; each call's time is the max
+    # over ranks, the value the whole job's units over those times
+    e2e = None
+    if hasattr(wl, "e2e_call"):
+        for _ in range(max(2, args.warmup)):  # first calls allocate pinned/device pools
+            wl.e2e_call()
+        torch.cuda.synchronize(dev)
+        times, nbytes = [], 0
+        for _ in range(args.steps):
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            nbytes = wl.e2e_call()
+            el = time.perf_counter() - t0
+            if dist is not None:
+                t = torch.tensor([el], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t[0])
+            times.append(el)
+        dg = _native.device_graph(wl.g, wl.f, dev)
+        e2e = {"value": wl.units_per_step * world * len(times) / sum(times), "unit": wl.unit,
+               "h2d_bytes_per_step": int(dg.device_bytes) * world,
+               "d2h_bytes_per_step": int(nbytes) * world,
+               "ms_per_call": [round(t * 1e3, 2) for t in times],
+               "path": "paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble) on every "
+                       "rank: graph upload, kernel, pinned D2H of the reference-dtype result "
+                       "arrays (4 particle-id chunks: each chunk's D2H overlaps the next "
+                       "kernel); time = max over ranks"}
     line = None
     if rank == 0:
-        # e2e through the public API with host buffers (graph upload + D2H)
-        e2e = None
-        if hasattr(wl, "e2e_call"):
-            for _ in range(max(2, args.warmup)):  # first calls allocate pinned/device pools
-                wl.e2e_call()
-            torch.cuda.synchronize(dev)
-            times, nbytes = [], 0
-            for _ in range(args.steps):
-                t0 = time.perf_counter()
-                nbytes = wl.e2e_call()
-                times.append(time.perf_counter() - t0)
-            dg = _native.device_graph(wl.g, wl.f, dev)
-            e2e = {"value": wl.units_per_step * len(times) / sum(times), "unit": wl.unit,
-                   "h2d_bytes_per_step": int(dg.device_bytes),
-                   "d2h_bytes_per_step": int(nbytes),
-                   "ms_per_call": [round(t * 1e3, 2) for t in times],
-                   "path": "paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble): graph "
-                           "upload, kernel, pinned D2H of the reference-dtype result arrays "
-                           "(4 particle-id chunks: each chunk's D2H overlaps the next kernel)"}
         line = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
