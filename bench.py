@@ -600,7 +600,7 @@ def main():
                "ms_per_call": [round(t * 1e3, 2) for t in times],
                "path": "paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble) on every "
                        "rank: graph upload, kernel, pinned D2H of the reference-dtype result "
-                       "arrays (4 particle-id chunks: each chunk's D2H overlaps the next "
+                       "arrays (5 particle-id chunks: each chunk's D2H overlaps the next "
                        "kernel); time = max over ranks"}
     line = None
     if rank == 0:
