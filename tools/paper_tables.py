@@ -106,6 +106,8 @@ def _chi2(h1, h2, min_count=20):
 
 
 for name, build, init, steps, n_nat, n_ref, cells in (
+        ("C1 star3 (driftless kernel)", lambda: workloads.star3(), lambda g: gs.AtVertex(0), 1000,
+         1_000_000_000, 100_000_000, 16),
         ("C2 hub64", workloads.hub64, lambda g: gs.PerEdgeUniform(2.0), 1000,
          1_000_000_000, 100_000_000, 8),
         ("C4 vascular", workloads.vascular,
@@ -114,7 +116,7 @@ for name, build, init, steps, n_nat, n_ref, cells in (
     if ONLY and ONLY != "4":
         break
     g, f = build()
-    grid = gs.EdgeGrid.uniform(g, cells)
+    grid = gs.EdgeGrid.uniform(g, cells, lengths=[3.0] * g.n_edges if g.is_star else None)
     res = {}
     for rng, n, seed in (("native", n_nat, 31), ("reference", n_ref, 32)):
         t0 = time.time()
