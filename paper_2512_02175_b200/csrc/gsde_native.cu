@@ -46,6 +46,7 @@ constexpr int kMinBlocksStar = 3;            // star-graph ensembles: <= 85 regi
 // trials: the compiler settles at 40 registers (48 warps / SM) under a 64-register
 // bound; the same kernel scheduled under a 51-register bound (5 blocks) ran 3% slower
 constexpr int kMinBlocksTrials = 4;
+constexpr int kTrialWaves = 4;  // trials grid: resident blocks x 4
 constexpr int kPriv = 8;       // lane-private M-histogram bins
 constexpr int kTrips = 14;     // ensemble: trips per iteration
 constexpr uint32_t kDomainEnsemble = 0u;
@@ -1013,11 +1014,11 @@ size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit, int o
 }
 
 template <class K>
-int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items) {
+int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items, int waves = 1) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t full = (int64_t)dev_info(device).sm_count * per_sm;
+  const int64_t full = (int64_t)dev_info(device).sm_count * per_sm * waves;
   const int64_t need = (n_items + kThreads - 1) / kThreads;
   return (int)(need < full ? (need < 1 ? 1 : need) : full);
 }
@@ -1156,7 +1157,13 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
                  : native_trials_kernel<decltype(cfg), false>;
     cudaError_t err = prepare(k, smem);
     if (err != cudaSuccess) return err;
-    return launch(k, smem, occupancy_grid(k, smem, d, n), s, g->nat, p, o, priv);
+    // four waves of blocks: with one resident wave and a static share per
+    // thread, the warp schedulers' favourites finished at about half time and
+    // the SMs ran on with ~34 of 48 warps (measured per-warp exit times); later
+    // waves refill the slots of early blocks (measured: 1 / 2 / 4 / 8 / 16
+    // waves 48.8 / 46.8 / 46.0 / 46.0 / 46.4 ms on C3).  A per-lane dynamic
+    // hand-out from a warp pool kept 40 registers but cost 7%.
+    return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, priv);
   });
 }
 
