@@ -353,7 +353,10 @@ __global__ void __launch_bounds__(256) step_batch_kernel(RefGraph<R> g, gsde_ste
 int grid_for(int64_t n, int device) {
   const int sms = dev_info(device).sm_count;
   int64_t blocks = (n + 255) / 256;
-  const int64_t cap = (int64_t)sms * 8;
+  // several waves of blocks (grid-stride, static shares): later blocks refill
+  // the slots of warps the schedulers favoured (8 -> 32 blocks per SM: C1
+  // 4.91e10 -> 5.13e10, hub64 1.18e10 -> 1.29e10 psteps/s, tools/ref_rate.py)
+  const int64_t cap = (int64_t)sms * 32;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return (int)blocks;
