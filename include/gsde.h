@@ -48,7 +48,8 @@ enum { GSDE_STREAM_NATIVE = 0, GSDE_STREAM_REFERENCE = 1, GSDE_STREAM_INJECT = 2
  * in that precision; NATIVE runs the production FP32 kernel itself (the
  * NATIVE stream's kernel with each proposal's normal and each exit uniform
  * taken from the injected rows in the reference's order, exit slots by the
- * reference's inverse CDF): ensembles only, no tabulated drift, no occ. */
+ * reference's inverse CDF): ensembles (without the occupation histogram)
+ * and vertex trials. */
 enum { GSDE_PREC_F32 = 0, GSDE_PREC_F64 = 1, GSDE_PREC_NATIVE = 2 };
 
 /* Initial placement codes (kernels.py:48-50). */

@@ -413,9 +413,9 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
   if (a->stream == GSDE_STREAM_NATIVE && a->n_steps > 0x7fffffffll)
     return set_error(GSDE_EINVAL, "ensemble: NATIVE stream supports n_steps < 2^31");
   const bool native_inj = a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE;
-  if (native_inj && (g->has_tab || o->occ))
-    return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE supports neither tabulated drifts "
-                                  "nor the occupation histogram");
+  if (native_inj && o->occ)
+    return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE does not sample the occupation "
+                                  "histogram");
   if (native_inj && (a->n_steps > 0x7fffffffll || a->inj_stride > 0x7fffffffll))
     return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE needs n_steps, inj_stride < 2^31");
   if (a->n_particles == 0) return GSDE_OK;
@@ -438,13 +438,15 @@ int gsde_vertex_trials(const gsde_graph *g, const gsde_trials *a, const gsde_tri
   int rc = check_stream_args(a->stream, a->precision, a->inj_raw, a->inj_normal, a->inj_stride,
                              "vertex_trials");
   if (rc) return rc;
-  if (a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE)
-    return set_error(GSDE_EINVAL, "%s: INJECT/NATIVE is an ensemble mode", "vertex_trials");
+  const bool native_inj = a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE;
+  if (native_inj && a->inj_stride > 0x7fffffffll)
+    return set_error(GSDE_EINVAL, "vertex_trials: INJECT/NATIVE needs inj_stride < 2^31");
   if (a->n_trials == 0) return GSDE_OK;
   DeviceGuard guard(g->device);
   const cudaStream_t s = (cudaStream_t)stream;
-  const cudaError_t err = a->stream == GSDE_STREAM_NATIVE ? launch_native_trials(g, *a, *o, s)
-                                                          : launch_ref_trials(g, *a, *o, s);
+  const cudaError_t err = (a->stream == GSDE_STREAM_NATIVE || native_inj)
+                              ? launch_native_trials(g, *a, *o, s)
+                              : launch_ref_trials(g, *a, *o, s);
   return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "vertex_trials launch");
 }
 

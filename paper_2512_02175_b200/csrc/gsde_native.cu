@@ -898,7 +898,8 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
 // fused exit counts per edge and M histogram including M = 0.
 template <class C, bool OUT>
 __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
-    native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv) {
+    native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv,
+                         InjParams q) {
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
@@ -911,7 +912,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   Lane<C> L;
   uint32_t pair = 0;
   uint64_t id = 0;
-  int32_t t_M = 0, t_ev = 0, t_tr = 0;  // per lane: <= ~1e4 trials x cap
+  int32_t t_M = 0, t_ev = 0, t_tr = 0, t_over = 0;  // per lane: <= ~1e4 trials x cap
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
     L.load_edge(T, O, C::STAR ? 0 : p.start_edge, p.sqdt, inf);
@@ -922,8 +923,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     L.trunc = false;
     L.steps_left = 1;  // (general: the sign carries a pending re-hit)
     pair = 0;
+    if constexpr (C::INJ) {  // the trial's own injected row, from draw 0
+      L.thr = q.thresh;
+      L.ved = q.vedges;
+      L.vor = q.vorient;
+      L.ir = q.raw + i * q.stride;
+      L.inn = q.normal + i * q.stride;
+      L.k = 0;
+      L.kmax = (int)q.stride;
+      L.over = false;
+    }
   };
   auto finish = [&]() {
+    if (C::INJ) t_over += L.over ? 1 : 0;
     if (OUT) {  // per-trial arrays (vertex_crossing_trials); the fused estimator skips them
       if (o.M) o.M[i] = L.M;
       if (o.edge) o.edge[i] = L.e;
@@ -951,9 +963,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   // a trial is one macro step started at the vertex: every trip is a vertex
   // trip, so the rare-path step functions run directly
   while (__any_sync(0xffffffffu, active)) {
-    const Block r = native_block(p, pair++, kDomainTrials, id);
-    float z0, z1;
-    box_muller(r.x, r.y, z0, z1);
+    Block r{0u, 0u, 0u, 0u};
+    float z0 = 0.0f, z1 = 0.0f;
+    if constexpr (!C::INJ) {  // (injected draws are taken per use inside the trips)
+      r = native_block(p, pair++, kDomainTrials, id);
+      box_muller(r.x, r.y, z0, z1);
+    }
     bool fin = false;
     if (active) fin = rare_trip<C, false>(L, G, T, O, p, z0, r.z);
     if (active && !fin) fin = rare_trip<C, false>(L, G, T, O, p, z1, r.w);
@@ -963,6 +978,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     warp_add_i64(&o.totals[0], t_M);
     warp_add_i64(&o.totals[1], t_ev);
     warp_add_i64(&o.totals[2], t_tr);
+    if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
   shared_flush(S, nb, o.m_hist, 0, nullptr);
   if (S.exit_priv && o.exit_counts) {
@@ -1062,9 +1078,9 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
     constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
     auto drift = [&](auto rf) -> cudaError_t {
       constexpr bool RF = decltype(rf)::value;
-      if (inj) {  // parity mode: no tabulated drift, no occupation sampling
+      if (inj) {  // parity mode: no occupation sampling
         if constexpr (!OCC) {
-          if (tab) return cudaErrorInvalidValue;
+          if (tab) return f(Cfg<ST, SM, true, RF, false, false, true>{});
           return zd ? f(Cfg<ST, SM, false, RF, false, true, true>{})
                     : f(Cfg<ST, SM, false, RF, false, false, true>{});
         }
@@ -1150,6 +1166,9 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   const size_t smem = smem_bytes(g, a.cap + 1, stage, priv, 0);
   const int d = g->device;
   const int64_t n = a.n_trials;
+  const bool inj = a.stream == GSDE_STREAM_INJECT;  // (precision GSDE_PREC_NATIVE)
+  const InjParams q{a.inj_raw,        a.inj_normal,       a.inj_stride,
+                    g->ref32.v_thresh, g->ref32.v_edges, g->ref32.v_orient};
   return dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, false,
                          [&](auto cfg) -> cudaError_t {
     const bool out = o.M || o.edge || o.x || o.trunc;
@@ -1163,8 +1182,9 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
     // waves refill the slots of early blocks (measured: 1 / 2 / 4 / 8 / 16
     // waves 48.8 / 46.8 / 46.0 / 46.0 / 46.4 ms on C3).  A per-lane dynamic
     // hand-out from a warp pool kept 40 registers but cost 7%.
-    return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, priv);
-  });
+    return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, priv,
+                  q);
+  }, inj);
 }
 
 cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,

@@ -571,7 +571,8 @@ def trials_device(graph, field, dt, n_trials, seed, vertex=0, max_splits=DEFAULT
     if inject is not None:
         raw, nrm = inject
         t.stream = _native.GSDE_STREAM_INJECT
-        t.precision = _native.GSDE_PREC_F64 if precision == "f64" else _native.GSDE_PREC_F32
+        t.precision = {"f64": _native.GSDE_PREC_F64, "f32": _native.GSDE_PREC_F32,
+                       "native": _native.GSDE_PREC_NATIVE}[precision]
         t.inj_raw, t.inj_normal, t.inj_stride = raw.data_ptr(), nrm.data_ptr(), raw.shape[1]
     s = stream if stream is not None else _native.cur_stream(dev)
     _native.check(_native.lib().gsde_vertex_trials(dg.handle, t, o, s))

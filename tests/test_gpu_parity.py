@@ -226,6 +226,42 @@ def test_inject_native_kernel_full_trajectories(case, n, steps, dt, init, K, fra
     assert (same & loose).mean() >= 0.995
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_inject_native_trials_kernel(seed):
+    """The production vertex-trials kernel (the C3 path) fed the reference's
+    draws: per trial M, exit edge and truncation identical to the C oracle,
+    exit positions within 1e-5 (FP32; rare near-ties allowed)."""
+    rng = np.random.default_rng(9100 + seed)
+    if seed == 0:
+        g, f = helpers.graph_for("star5_linear")
+    elif seed % 2:
+        k = int(rng.integers(2, 9))
+        spec = dict(edges=[(0, None, float("inf"))] * k, weights=None,
+                    drift=[("constant", float(rng.uniform(-40, 5))) for _ in range(k)],
+                    sigma=[float(rng.uniform(0.5, 2.0)) for _ in range(k)])
+        g, f = cases.build(spec, gs)
+    else:
+        spec = cases._random_general(int(rng.integers(4, 25)), int(rng.integers(0, 6)),
+                                     int(rng.integers(0, 1 << 30)))
+        g, f = cases.build(spec, gs)
+    v = 0 if g.is_star else int(rng.integers(0, g.n_vertices))
+    dt = float(10 ** rng.uniform(-4, -1.5))
+    cap = int(rng.choice([10, 100]))
+    n = 20_000
+    res = engine.trials_device(g, f, dt, n, seed, vertex=v, max_splits=cap,
+                               inject=_inject_tensors(seed, n, 2 * cap + 4), precision="native")
+    assert int(res["totals"][3]) == 0
+    e0, x0 = engine._trial_start(g, v)
+    o = oracle.vertex_trials(oracle.OracleGraph(g, f), seed, n, dt, e0, x0, cap)
+    M, ex, tr = (res[k].cpu().numpy() for k in ("M", "edge", "trunc"))
+    x = res["x"].cpu().numpy()
+    same = (M == o["M"]) & (ex == o["exit_edges"]) & (tr == o["truncated"])
+    close = np.abs(x - o["exit_positions"]) <= 1e-5 * np.maximum(np.abs(o["exit_positions"]),
+                                                                 np.sqrt(dt))
+    assert same.mean() >= 0.995, same.mean()
+    assert (same & close).mean() >= 0.99, (same & close).mean()
+
+
 def test_histogram_kernel_matches_oracle():
     rng = np.random.default_rng(3)
     g, _ = cases.build("hub8", gs)
