@@ -35,6 +35,11 @@ for gg, ff, init, n in ((*cases.build("star3_bm", gs), gs.AtVertex(0), 2000),
     inj = (torch.as_tensor(raw.view(np.int64)).cuda(), torch.as_tensor(nrm).cuda())
     cfg = gs.SimulationConfig(dt=1e-3, n_steps=60, n_particles=n, seed=3, initial=init)
     engine.ensemble_device(gg, ff, cfg, inject=inj, precision="native")
+gt, ft = cases.build("random_general", gs)  # trials, incl. tabulated drifts
+raw = rs.integers(0, 2**63, size=(3000, 210), dtype=np.int64).view(np.uint64)
+inj = (torch.as_tensor(raw.view(np.int64)).cuda(),
+       torch.as_tensor(rs.standard_normal((3000, 210))).cuda())
+engine.trials_device(gt, ft, 1e-3, 3000, 3, max_splits=100, inject=inj, precision="native")
 gp, fp = cases.build("path3", gs)
 gridp = gs.EdgeGrid(counts=np.array([3, 1]), lengths=gp.edge_length)
 fvm.fvm_steps_device(gp, fp, gridp, np.linspace(1, 2, 4), 20, 0.5 * fvm.stability_limit(gp, fp, gridp))
