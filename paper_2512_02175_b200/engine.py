@@ -326,6 +326,13 @@ _PIPELINE_MIN = 1 << 22
 _COPY_STREAMS: dict = {}  # device -> (copy stream, second launch stream)
 
 
+def _chunk_bounds(n: int) -> np.ndarray:
+    """Particle-id boundaries of run_ensemble's chunks: [0, ..., n]."""
+    bounds = np.concatenate([[0], np.cumsum(np.floor(np.array(_CHUNKS) * n).astype(np.int64))])
+    bounds[-1] = n
+    return bounds
+
+
 def _ensemble_to_host(graph, field, config):
     """run_ensemble's device work + transfers: per-particle arrays land in
     pinned host memory; large runs are split by global particle id (results
@@ -347,8 +354,7 @@ def _ensemble_to_host(graph, field, config):
     side.wait_stream(compute)  # whatever the caller queued comes first
     hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
              for k in names]
-    bounds = np.concatenate([[0], np.cumsum(np.floor(np.array(_CHUNKS) * n).astype(np.int64))])
-    bounds[-1] = n
+    bounds = _chunk_bounds(n)
     parts = []
     for c, (lo, hi) in enumerate(zip(bounds[:-1], bounds[1:])):
         if hi <= lo:
