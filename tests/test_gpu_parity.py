@@ -198,6 +198,8 @@ def test_inject_f32_full_trajectories_c1():
     # general, L2 tables; 200 FP32 steps of advection accumulate rounding: the
     # reference-order FP32 stepper (precision="f32") measures the same 96.4%
     ("vascular_small", 10_000, 200, 1e-3, ("uniform", 2.0), 1200, 0.95),
+    # tabulated + linear + constant drifts, a zero-weight slot, cap 5 (truncations)
+    ("star4_mixed", 10_000, 300, 1e-2, ("uniform", 0.2), 1000, 0.99),
 ])
 def test_inject_native_kernel_full_trajectories(case, n, steps, dt, init, K, frac):
     """The north-star contract on the PRODUCTION kernel: the native FP32
@@ -207,12 +209,14 @@ def test_inject_native_kernel_full_trajectories(case, n, steps, dt, init, K, fra
     and crossing counts exact, positions within 1e-5 (FP32 rounding may flip
     a rare near-tie)."""
     g, f = helpers.graph_for(case)
+    cap = 5 if case == "star4_mixed" else 100
     cfg = gs.SimulationConfig(dt=dt, n_steps=steps, n_particles=n, seed=20251202,
-                              initial=helpers.initial_for(init))
+                              initial=helpers.initial_for(init), max_splits_per_step=cap)
     out = engine.ensemble_device(g, f, cfg, inject=_inject_tensors(20251202, n, K),
                                  precision="native")
     assert int(out["totals"][3]) == 0  # no particle ran past its injected draws
-    o = _oracle_run(g, f, 20251202, n, steps, dt, helpers.oracle_init(init, g))
+    o = _oracle_run(g, f, 20251202, n, steps, dt, helpers.oracle_init(init, g), cap=cap)
+    np.testing.assert_array_equal(out["m_hist"].cpu().numpy() > 0, o["m_histogram"] > 0)
     e, c = out["edge"].cpu().numpy(), out["crossings"].cpu().numpy()
     x = out["x"].cpu().numpy()
     same = (e == o["edges"]) & (c == o["crossings"])
@@ -224,6 +228,22 @@ def test_inject_native_kernel_full_trajectories(case, n, steps, dt, init, K, fra
     assert (same & close).mean() >= frac
     loose = np.abs(x - o["positions"]) <= 1e-3 * np.maximum(np.abs(o["positions"]), np.sqrt(dt))
     assert (same & loose).mean() >= 0.995
+
+
+def test_inject_native_kernel_mirror_wall():
+    """Star mirror wall (reflect_at) in the production kernel under injected draws."""
+    g, f = helpers.graph_for("star3_drift")
+    n, steps, dt, wall = 4_000, 200, 1e-3, 0.05
+    cfg = gs.SimulationConfig(dt=dt, n_steps=steps, n_particles=n, seed=11, reflect_at=wall)
+    out = engine.ensemble_device(g, f, cfg, inject=_inject_tensors(11, n, 2400),
+                                 precision="native")
+    assert int(out["totals"][3]) == 0
+    o = _oracle_run(g, f, 11, n, steps, dt, (0, 0, 0.0, 0.0), refl=wall)
+    e, c, x = (out[k].cpu().numpy() for k in ("edge", "crossings", "x"))
+    same = (e == o["edges"]) & (c == o["crossings"])
+    close = np.abs(x - o["positions"]) <= 1e-5 * np.maximum(np.abs(o["positions"]), np.sqrt(dt))
+    assert same.mean() >= 0.995 and (same & close).mean() >= 0.99, (same.mean(), close.mean())
+    assert x.max() <= wall
 
 
 @pytest.mark.parametrize("seed", range(6))
