@@ -626,7 +626,7 @@ def main():
             },
             "crossings_per_pstep": c_per,
         }
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # (the contract's CPU leg: rank 0 at N=1 only)
             line["cpu_baseline"] = cpu_baseline(wl)
         if not args.no_extras and world == 1:
             extras = {}
