@@ -52,22 +52,30 @@ class Workload:
 
 class Ensemble(Workload):
     def __init__(self, name, desc, build, n_per_gpu, n_steps, dt, initial, grid_fn, rank=0,
-                 world=1):
+                 world=1, rng="native"):
         super().__init__(rank, world)
         import paper_2512_02175_b200 as gs
 
         self.name, self.desc = name, desc
+        self.build = build
         self.g, self.f = build()
         self.n, self.n_steps, self.dt = n_per_gpu, n_steps, dt
         self.initial = initial(self.g)
         self.grid = grid_fn(self.g)
+        self.rng = rng
         self.cfg = gs.SimulationConfig(dt=dt, n_steps=n_steps, n_particles=n_per_gpu * world,
-                                       seed=20251202, initial=self.initial, rng="native")
+                                       seed=20251202, initial=self.initial, rng=rng)
         self.units_per_step = n_per_gpu * n_steps  # per GPU
+
+    def build_ref(self, R):
+        """The same graph built through the reference package ``R``."""
+        return self.build(api=R)
 
     def config(self):
         return {"workload": self.desc, "n_particles_per_gpu": self.n, "n_steps": self.n_steps,
-                "dt": self.dt, "graph_edges": self.g.n_edges, "rng": "native (FP32, Philox4x32-10)"}
+                "dt": self.dt, "graph_edges": self.g.n_edges,
+                "rng": ("native (FP32, Philox4x32-10)" if self.rng == "native" else
+                        "reference (the reference's Philox4x32-10 + AS241 streams, FP64)")}
 
     def launch(self, stream):
         from paper_2512_02175_b200 import engine
@@ -85,12 +93,33 @@ class Ensemble(Workload):
         return int(res["totals"][0])
 
     def e2e_call(self):
+        """One public-API call with host buffers; returns D2H bytes.  N = 1:
+        ``run_ensemble`` (the drop-in call).  N > 1: the sharded job,
+        ``parallel.run_ensemble_distributed(particles=True)`` -- every rank
+        simulates its global-id shard, copies its per-particle arrays to host
+        memory, and the fused estimators are merged with one all-reduce."""
         import paper_2512_02175_b200 as gs
+        from paper_2512_02175_b200 import parallel
 
         self.g._device.clear()  # inputs travel every step: graph + field upload
-        r = gs.run_ensemble(self.g, self.f, self.cfg_single())
-        d2h = sum(a.nbytes for a in (r.edges, r.positions, r.crossings, r.crossing_events))
-        return d2h + r.stats.m_histogram.nbytes
+        if self.world == 1:
+            r = gs.run_ensemble(self.g, self.f, self.cfg_single())
+            d2h = sum(a.nbytes for a in (r.edges, r.positions, r.crossings, r.crossing_events))
+            return d2h + r.stats.m_histogram.nbytes + 4 * 8
+        r = parallel.run_ensemble_distributed(self.g, self.f, self.cfg, grid=self.grid,
+                                              particles=True)
+        d2h = sum(a.nbytes for a in r.particles.values())
+        return d2h + r.m_histogram.nbytes + 4 * 8 + r.edge_counts.nbytes + r.histogram.nbytes
+
+    def e2e_path(self):
+        if self.world == 1:
+            return ("paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble): graph upload, "
+                    "kernel, pinned D2H of the reference-dtype result arrays (5 particle-id "
+                    "chunks: each chunk's D2H overlaps the next kernel)")
+        return ("paper_2512_02175_b200.parallel.run_ensemble_distributed(particles=True): per "
+                "rank graph upload, its global-id shard through the chunked run_ensemble "
+                "pipeline (per-particle arrays to host), one all-reduce of the fused "
+                "estimators, D2H of the merged estimators; time = max over ranks")
 
     def cfg_single(self):
         import dataclasses
@@ -134,6 +163,11 @@ class Trials(Workload):
         self.n, self.dts = n_per_dt, tuple(dts)
         self.units_per_step = n_per_dt * len(dts)
 
+    def build_ref(self, R):
+        from paper_2512_02175_b200 import workloads
+
+        return workloads.star5("linear", api=R)
+
     def config(self):
         return {"workload": self.desc, "n_trials_per_dt_per_gpu": self.n, "dts": list(self.dts)}
 
@@ -150,6 +184,28 @@ class Trials(Workload):
         import torch
 
         return torch.cat([res["exit_counts"], res["m_hist"], res["totals"]])
+
+    def e2e_call(self):
+        """The public exit-probability API with host results: N = 1
+        ``analysis.exit_probability_experiment`` over the dt sweep (fused exit
+        counts, no per-trial arrays); N > 1 ``parallel.exit_counts_distributed``
+        per dt (global trial-id shards, one all-reduce each)."""
+        from paper_2512_02175_b200 import analysis, parallel
+
+        self.g._device.clear()
+        if self.world == 1:
+            analysis.exit_probability_experiment(self.g, self.f, self.dts, self.n, 11)
+        else:
+            for i, dt in enumerate(self.dts):
+                parallel.exit_counts_distributed(self.g, self.f, dt, self.n * self.world, 11 + i)
+        return len(self.dts) * 8 * (self.g.n_edges + 101 + 4)
+
+    def e2e_path(self):
+        if self.world == 1:
+            return ("paper_2512_02175_b200.analysis.exit_probability_experiment: graph upload, "
+                    "one fused vertex-trials launch per dt, D2H of exit counts + M histogram")
+        return ("paper_2512_02175_b200.parallel.exit_counts_distributed per dt: global "
+                "trial-id shards, one all-reduce of the fused counts; time = max over ranks")
 
     def crossings(self, res):
         return int(res["totals"].view(-1, 4)[:, 0].sum())
@@ -247,6 +303,14 @@ def make_workload(name, rank, world):
             _vascular_cached, 100_000_000 // world, 100, 1e-3,
             lambda g: gs.PerEdgeUniform(float(g.edge_length.max())),
             lambda g: gs.EdgeGrid.uniform(g, 8), rank, world)
+    if name == "star3_ref":  # the bit-compatible FP64 reference stream on C1-throughput
+        return Ensemble(
+            "star3_ref", "C1-throughput in the reference's own streams (rng='reference': "
+            "Philox4x32-10 + AS241 normals, FP64, inverse-CDF exits; edge ids / crossings "
+            "bit-identical to graphsde): 3-edge Brownian star, 1.6e7 particles/GPU x 1000 steps",
+            workloads.star3, 16_000_000, 1000, 1e-3, lambda g: gs.AtVertex(0),
+            lambda g: gs.EdgeGrid.uniform(g, 16, lengths=[3.0] * 3), rank, world,
+            rng="reference")
     if name == "star5_trials":
         return Trials(rank, world)
     if name == "fvm":
@@ -254,16 +318,17 @@ def make_workload(name, rank, world):
     raise SystemExit(f"unknown workload {name}")
 
 
-_VASC = None
+_VASC = {}
 
 
-def _vascular_cached():
-    global _VASC
-    if _VASC is None:
+def _vascular_cached(api=None):
+    """The C4 network (this package's objects, or the reference's with ``api``)."""
+    key = None if api is None else api.__name__
+    if key not in _VASC:
         from paper_2512_02175_b200 import workloads
 
-        _VASC = workloads.vascular()
-    return _VASC
+        _VASC[key] = workloads.vascular(api=api)
+    return _VASC[key]
 
 
 # ----------------------------------------------------------------------------
@@ -374,21 +439,102 @@ def load_traffic(workload):
 
 
 # ----------------------------------------------------------------------------
-#: Measured in the build container (8-core Xeon, AVX-512; C1, 4e5 particles x
-#: 1000 steps, warm JIT, 8 threads, three runs each): the reference's own numba
-#: kernels (fastmath) run 5.4e8-6.4e8 psteps/s, the strict-IEEE C port 3.2e8-3.6e8
-#: (an -O3 -march=native -ffast-math build of the port: 3.6e8-3.8e8).  The port
-#: is the traveling stand-in (the Python reference cannot run on the GPU box), so
-#: CPU ratios computed against it overstate the speed-up vs the reference by
-#: about this factor.
-REFERENCE_OVER_PORT = 5.9e8 / 3.4e8
+# the reference's own CPU path (numba), installed unmodified under baseline/_ref
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def cpu_baseline(wl, seconds=12.0):
-    """Oracle (C port of the reference algorithm, OpenMP over particle chunks,
-    all host threads) on a bounded sample of the same workload."""
-    from oracle import oracle
+def reference_package():
+    """``(graphsde, None)``: the UNMODIFIED reference package, installed with
+    ``pip install --no-index --no-build-isolation --no-deps --target
+    baseline/_ref <copy of /root/reference/pkg>`` (its numba / numpy / scipy
+    dependencies are already in the image; pip's resolver only fails on the
+    pins), running its own numba CPU kernels -- or ``(None, reason)``."""
+    if not os.path.isdir(os.path.join(REF_DIR, "graphsde")):
+        return None, "baseline/_ref/graphsde is not installed"
+    # the reference's kernels are @njit(cache=True): keep the JIT cache off the repo copy
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "gsde_numba_cache"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(1, REF_DIR)
+    try:
+        import graphsde
+        import graphsde.graphfile  # noqa: F401  (not re-exported by graphsde/__init__)
+    except Exception as exc:  # numba missing, ...
+        return None, f"import graphsde failed: {exc!r}"
+    return graphsde, None
 
+
+class RefRunner:
+    """One bench workload on the reference's public API and stock code path
+    (``graphsde.run_ensemble`` / ``graphsde.vertex_crossing_trials``, numba
+    ``prange`` over all host threads): same graph (built through the
+    reference's own ``build_graph`` / graph-file parser), seed, dt, steps and
+    initial law; a bounded particle / trial sample."""
+
+    def __init__(self, wl, R):
+        import dataclasses
+
+        self.R = R
+        self.threads = int(R.engine.available_workers())
+        self.unit = wl.unit
+        self.trials = isinstance(wl, Trials)
+        if self.trials:
+            self.g, self.f = wl.build_ref(R)
+            self.dts = wl.dts
+            self.desc = "graphsde.vertex_crossing_trials"
+        else:
+            self.g, self.f = wl.build_ref(R)
+            init = wl.initial
+            self.initial = getattr(R, type(init).__name__)(*dataclasses.astuple(init))
+            self.n_steps, self.dt = wl.n_steps, wl.dt
+            self.desc = "graphsde.run_ensemble"
+
+    def run(self, n):
+        """n particles (ensembles) / n trials split over the dts; returns units done."""
+        R = self.R
+        if self.trials:
+            per = max(1, int(n) // len(self.dts))
+            for i, dt in enumerate(self.dts):
+                R.vertex_crossing_trials(self.g, self.f, dt, per, 11 + i, workers=self.threads)
+            return per * len(self.dts)
+        n = max(1, int(n))
+        cfg = R.SimulationConfig(dt=self.dt, n_steps=self.n_steps, n_particles=n,
+                                 seed=20251202, initial=self.initial, workers=self.threads)
+        R.run_ensemble(self.g, self.f, cfg)
+        return n * self.n_steps
+
+    def per_unit(self):
+        return len(self.dts) if self.trials else self.n_steps
+
+    def sized(self, seconds):
+        """(n, rate): JIT warm-up (compile or cache load) excluded, then a
+        ~1 s calibration, then n sized for ``seconds`` of CPU work."""
+        t0 = time.perf_counter()
+        self.run(4096 if self.trials else 256)
+        self.jit_s = time.perf_counter() - t0
+        n = 4096 * self.threads * (4 if self.trials else 1)
+        while True:
+            t0 = time.perf_counter()
+            units = self.run(n)
+            el = time.perf_counter() - t0
+            if el > 0.5 or n > 1e9:
+                break
+            n *= 4
+        rate = units / el
+        per = self.per_unit()
+        return max(n, int(rate * seconds / per)), rate
+
+    def sample_desc(self, n):
+        if self.trials:
+            per = max(1, int(n) // len(self.dts))
+            return (f"{per} trials per dt x {len(self.dts)} dts via {self.desc} (numba, "
+                    f"{self.threads} threads, baseline/_ref)")
+        return (f"{int(n)} particles x {self.n_steps} steps via {self.desc} (numba, "
+                f"{self.threads} threads, baseline/_ref)")
+
+
+def _port_baseline(wl, seconds, why):
+    """Fallback when the reference package cannot run: the C restatement of its
+    kernels in oracle/ (strict IEEE, OpenMP over the reference's chunks)."""
     threads = os.cpu_count() or 1
     if isinstance(wl, Trials):
         t0 = time.perf_counter()
@@ -396,10 +542,9 @@ def cpu_baseline(wl, seconds=12.0):
         rate = n_cal / max(time.perf_counter() - t0, 1e-6)
         t0 = time.perf_counter()
         n = wl.cpu_run(int(min(max(rate * seconds, n_cal), 2e9)), threads)
-        dt = time.perf_counter() - t0
-        return {"value": n / dt, "unit": wl.unit, "cores": threads, "kind": "port",
-                "sample": f"{n} trials (oracle/gsde_oracle.c, {threads} threads)",
-                "reference_over_port_measured_in_container": REFERENCE_OVER_PORT}
+        return {"value": n / (time.perf_counter() - t0), "unit": wl.unit, "cores": threads,
+                "kind": "port", "sample": f"{n} trials (oracle/gsde_oracle.c, {threads} threads)",
+                "reference_unavailable": why}
     run, units, desc = wl.cpu_sample(20_000)
     t0 = time.perf_counter()
     run(threads)
@@ -407,29 +552,55 @@ def cpu_baseline(wl, seconds=12.0):
     run, units, desc = wl.cpu_sample(20_000 * max(1.0, rate * seconds / units))
     t0 = time.perf_counter()
     run(threads)
-    dt = time.perf_counter() - t0
-    return {"value": units / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{desc} (oracle/gsde_oracle.c, {threads} threads)",
-            "reference_over_port_measured_in_container": REFERENCE_OVER_PORT}
+    return {"value": units / (time.perf_counter() - t0), "unit": UNIT, "cores": threads,
+            "kind": "port", "sample": f"{desc} (oracle/gsde_oracle.c, {threads} threads)",
+            "reference_unavailable": why}
+
+
+def cpu_baseline(wl, seconds=12.0):
+    """The reference's own CPU path (numba, all host threads) timed on a
+    bounded sample of the same workload; the C port only if it cannot run."""
+    R, why = reference_package()
+    if R is None:
+        return _port_baseline(wl, seconds, why)
+    rr = RefRunner(wl, R)
+    n, _ = rr.sized(seconds)
+    t0 = time.perf_counter()
+    units = rr.run(n)
+    el = time.perf_counter() - t0
+    return {"value": units / el, "unit": wl.unit, "cores": rr.threads, "kind": "reference",
+            "sample": rr.sample_desc(n), "seconds": round(el, 2),
+            "jit_s_excluded": round(rr.jit_s, 2)}
 
 
 def run_reference_arm(args, rank, world):
+    """``--impl reference``: the reference's own CPU implementation (numba, all
+    host threads; rank 0 only), each step a ~2 s bounded sample of the same
+    workload."""
     if rank != 0:
         return
     wl = make_workload(args.workload, 0, 1)
-    base = cpu_baseline(wl, seconds=2.0)  # calibrates a ~2 s step
-    rate = base["value"]
-    from oracle import oracle  # noqa: F401
-
-    threads = os.cpu_count() or 1
-    if isinstance(wl, Trials):
-        n = max(len(wl.dts), int(rate * 2.0))
-        units = max(1, n // len(wl.dts)) * len(wl.dts)
-        step = lambda: wl.cpu_run(n, threads)
-        sample = f"{units} trials per step over dt = {', '.join(f'{d:g}' for d in wl.dts)}"
+    R, why = reference_package()
+    if R is None:  # the port stands in, and the line says so
+        base = _port_baseline(wl, 2.0, why)
+        threads = base["cores"]
+        if isinstance(wl, Trials):
+            n = max(len(wl.dts), int(base["value"] * 2.0))
+            units = max(1, n // len(wl.dts)) * len(wl.dts)
+            step = lambda: wl.cpu_run(n, threads)
+            sample = f"{units} trials per step (oracle port)"
+        else:
+            run, units, sample = wl.cpu_sample(max(4096, base["value"] * 2.0 / wl.n_steps))
+            step = lambda: run(threads)
+        kind = "port"
     else:
-        run, units, sample = wl.cpu_sample(max(4096, rate * 2.0 / wl.n_steps))
-        step = lambda: run(threads)
+        rr = RefRunner(wl, R)
+        n, _ = rr.sized(2.0)
+        threads = rr.threads
+        units = max(1, n // len(rr.dts)) * len(rr.dts) if rr.trials else n * rr.n_steps
+        step = lambda: rr.run(n)
+        sample = rr.sample_desc(n)
+        kind = "reference"
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
@@ -442,14 +613,15 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": dict(wl.config(), sample=sample,
+        "config": dict(wl.config(), sample=sample, same_workload_bounded_sample=True,
                        rng="reference streams (Philox4x32-10 + AS241, FP64)"),
-        "cpu_baseline": {"value": value, "unit": wl.unit, "cores": threads, "kind": "port",
-                         "sample": f"{sample} (oracle/gsde_oracle.c: C restatement of the "
-                                   "reference numba kernels; reference is Python)"},
+        "cpu_baseline": {"value": value, "unit": wl.unit, "cores": threads, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": wl.unit, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if R is None:
+        line["reference_unavailable"] = why
     print(json.dumps(line), flush=True)
 
 
@@ -511,6 +683,66 @@ def time_workload(wl, steps, warmup, dist, torch, dev, flush_buf, clocks_index=N
     return total, kern, res, launches, (sampler.summary() if sampler else None)
 
 
+def measure_e2e(wl, steps, warmup, dist, torch, dev, world):
+    """``e2e``: the workload's public-API call with host buffers (graph
+    upload, kernels, D2H of the result), every rank at once; each call's time
+    is the max over ranks, the value the whole job's units over those times."""
+    from paper_2512_02175_b200 import _native
+
+    for _ in range(max(2, warmup)):  # first calls allocate pinned / device pools
+        wl.e2e_call()
+    torch.cuda.synchronize(dev)
+    times, nbytes = [], 0
+    for _ in range(steps):
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        nbytes = wl.e2e_call()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t[0])
+        times.append(el)
+    dg = _native.device_graph(wl.g, wl.f, dev)
+    return {"value": wl.units_per_step * world * len(times) / sum(times), "unit": wl.unit,
+            "h2d_bytes_per_step": int(dg.device_bytes) * world,
+            "d2h_bytes_per_step": int(nbytes) * world,
+            "ms_per_call": [round(t * 1e3, 2) for t in times], "path": wl.e2e_path()}
+
+
+def extra_line(name, torch, dev, flush_buf, peaks, peak_ops, with_cpu):
+    """One secondary workload at N = 1: device-timed value + roofline, e2e
+    through its public API, and the reference CPU path beside it."""
+    w2 = make_workload(name, 0, 1)
+    t2, k2, r2, l2, _ = time_workload(w2, 3, 2, None, torch, dev, flush_buf)
+    rate2 = w2.units_per_step * 3 / t2
+    if name == "fvm":
+        bpc = FVM_BYTES_PER_CELL_STEP
+        return {
+            "value": rate2, "unit": w2.unit, "config": w2.config(), "gpu_launches": int(l2),
+            "bytes_per_cell_step": bpc, "achieved_gbs": rate2 * bpc / 1e9,
+            "frac_of_hbm_peak": rate2 * bpc / 1e9 / float(peaks.get("hbm_gbs", 7700)),
+            "note": "working set (~40 MB) is L2-resident across steps",
+            "cpu_baseline": {"value": w2.cpu_rate(), "unit": w2.unit, "cores": 1,
+                             "kind": "port",
+                             "sample": "10 steps, oracle/gsde_oracle.c orc_fvm_steps (single "
+                                       "thread, like the reference's numba stepper)"}}
+    c2 = w2.crossings(r2) / w2.units_per_step
+    out = {"value": rate2, "unit": w2.unit, "config": w2.config(), "step_ms": list(STEP_MS),
+           "gpu_launches": int(l2), "crossings_per_unit": c2,
+           "roofline_frac": w2.units_per_step * 3 / k2 * lane_ops_per_pstep(c2) / peak_ops}
+    if getattr(w2, "rng", "native") != "native":
+        out["roofline_frac"] = None
+        out["roofline_note"] = ("FP64 reference stream (AS241 normals, strict IEEE): the FP32 "
+                                "lane-op work model does not apply")
+    if hasattr(w2, "e2e_call"):
+        out["e2e"] = measure_e2e(w2, 3, 2, None, torch, dev, 1)
+    if with_cpu:
+        out["cpu_baseline"] = cpu_baseline(w2, seconds=8.0)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -518,7 +750,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="star3",
-                    choices=["star3", "hub64", "star5_trials", "vascular", "fvm"])
+                    choices=["star3", "hub64", "star5_trials", "vascular", "fvm", "star3_ref"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -546,6 +778,8 @@ def main():
         import torch.distributed as tdist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator setup (nranks, NVLS / NVLink transport) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         if shared:
             tdist.init_process_group("gloo")
         else:
@@ -573,42 +807,16 @@ def main():
     kern_rate = wl.units_per_step * args.steps / kern  # per GPU, kernel only
     achieved = kern_rate * w_ops
 
-    # e2e through the public API with host buffers (graph upload + D2H): every
-    # rank runs its per-GPU share concurrently; each call's time is the max
-    # over ranks, the value the whole job's units over those times
-    e2e = None
-    if hasattr(wl, "e2e_call"):
-        for _ in range(max(2, args.warmup)):  # first calls allocate pinned/device pools
-            wl.e2e_call()
-        torch.cuda.synchronize(dev)
-        times, nbytes = [], 0
-        for _ in range(args.steps):
-            if dist is not None:
-                dist.barrier()
-            t0 = time.perf_counter()
-            nbytes = wl.e2e_call()
-            el = time.perf_counter() - t0
-            if dist is not None:
-                t = torch.tensor([el], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                el = float(t[0])
-            times.append(el)
-        dg = _native.device_graph(wl.g, wl.f, dev)
-        e2e = {"value": wl.units_per_step * world * len(times) / sum(times), "unit": wl.unit,
-               "h2d_bytes_per_step": int(dg.device_bytes) * world,
-               "d2h_bytes_per_step": int(nbytes) * world,
-               "ms_per_call": [round(t * 1e3, 2) for t in times],
-               "path": "paper_2512_02175_b200.run_ensemble (C-ABI gsde_ensemble) on every "
-                       "rank: graph upload, kernel, pinned D2H of the reference-dtype result "
-                       "arrays (5 particle-id chunks: each chunk's D2H overlaps the next "
-                       "kernel); time = max over ranks"}
+    e2e = measure_e2e(wl, args.steps, args.warmup, dist, torch, dev, world) \
+        if hasattr(wl, "e2e_call") else None
     line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
             "step_ms": list(STEP_MS),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if getattr(wl, "rng", "native") == "native" else "f64",
             "data": "synthetic (seeded graph generators, random streams; no external data)",
             "config": dict(wl.config(), parallelism=f"particle-sharded x{world}",
                            l2="flushed between steps (256 MiB write)"),
@@ -629,35 +837,15 @@ def main():
         if not args.no_cpu and world == 1:  # (the contract's CPU leg: rank 0 at N=1 only)
             line["cpu_baseline"] = cpu_baseline(wl)
         if not args.no_extras and world == 1:
-            extras = {}
-            for name in ("hub64", "star5_trials", "vascular", "fvm"):
-                if name == args.workload:
-                    continue
-                w2 = make_workload(name, 0, 1)
-                t2, k2, r2, _, _ = time_workload(w2, 3, 2, None, torch, dev, flush_buf)
-                rate2 = w2.units_per_step * 3 / t2
-                if name == "fvm":
-                    bpc = FVM_BYTES_PER_CELL_STEP
-                    extras[name] = {
-                        "value": rate2, "unit": w2.unit, "config": w2.config(),
-                        "bytes_per_cell_step": bpc, "achieved_gbs": rate2 * bpc / 1e9,
-                        "frac_of_hbm_peak": rate2 * bpc / 1e9 / float(peaks.get("hbm_gbs", 7700)),
-                        "note": "working set (~40 MB) is L2-resident across steps",
-                        "cpu_baseline": {"value": w2.cpu_rate(), "unit": w2.unit, "cores": 1,
-                                         "kind": "port",
-                                         "sample": "10 steps, oracle/gsde_oracle.c "
-                                                   "orc_fvm_steps (single thread, like the "
-                                                   "reference)"}}
-                    continue
-                c2 = w2.crossings(r2) / w2.units_per_step
-                extras[name] = {"value": rate2, "unit": w2.unit, "config": w2.config(),
-                                "step_ms": list(STEP_MS), "crossings_per_unit": c2,
-                                "roofline_frac": rate2 * lane_ops_per_pstep(c2) / peak_ops}
-            line["workloads"] = extras
+            line["workloads"] = {
+                name: extra_line(name, torch, dev, flush_buf, peaks, peak_ops, not args.no_cpu)
+                for name in ("hub64", "star5_trials", "vascular", "star3_ref", "fvm")
+                if name != args.workload}
     if not args.no_extras:
         # C5 strong scaling on every rank (a collective run): fixed 1e10 psteps per step
         w5 = make_workload("vascular_c5", rank, world)
         t5, _, r5, _, _ = time_workload(w5, 3, 2, dist, torch, dev, flush_buf)
+        e5 = measure_e2e(w5, 3, 2, dist, torch, dev, world) if world > 1 else None
         if rank == 0:
             rate5 = w5.units_per_step * world * 3 / t5
             c5 = w5.crossings(r5) / w5.units_per_step
@@ -665,7 +853,9 @@ def main():
                 "value": rate5, "unit": w5.unit, "scaling": "strong", "n_gpus": world,
                 "config": dict(w5.config(), parallelism=f"particle-sharded x{world}"),
                 "step_ms": list(STEP_MS), "crossings_per_unit": c5,
-                "roofline_frac": rate5 / world * lane_ops_per_pstep(c5) / peak_ops}
+                "roofline_frac": rate5 / world * lane_ops_per_pstep(c5) / peak_ops,
+                "e2e": e5 if e5 is not None else line.get("workloads", {}).get(
+                    "vascular", {}).get("e2e")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -228,13 +228,16 @@ class DeviceGraph:
 
 
 def device_graph(graph, field, device=None) -> DeviceGraph:
-    """Cached upload of (graph, field) to ``device``."""
+    """Cached upload of (graph, field) to ``device``: one entry per device --
+    the most recent field (a sweep that builds a new field per point frees
+    the previous point's device arena instead of keeping one per field)."""
     _, device = torch_cuda(device)
     cache = graph._device
-    key = ("dg", id(field), device)
+    key = ("dg", device)
     hit = cache.get(key)
     if hit is not None and hit[0] is field:
         return hit[1]
+    cache.pop(key, None)  # drop the old handle first: its arena returns to the pool
     dg = DeviceGraph(graph, field, device)
     cache[key] = (field, dg)
     return dg

@@ -367,6 +367,8 @@ int gsde_graph_destroy(gsde_graph *g) {
   cudaError_t err = cudaDeviceSynchronize();
   if (err == cudaSuccess && !arena_pool().give(g->device, g->arena, (size_t)g->arena_bytes))
     err = cudaFree(g->arena);
+  for (cudaEvent_t ev : g->work_done)
+    if (ev) cudaEventDestroy(ev);
   delete g;
   return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "graph_destroy");
 }
@@ -412,6 +414,10 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
   if (rc) return rc;
   if (a->stream == GSDE_STREAM_NATIVE && a->n_steps > 0x7fffffffll)
     return set_error(GSDE_EINVAL, "ensemble: NATIVE stream supports n_steps < 2^31");
+  // NATIVE stream ids carry the block-counter carry in bits 48.. (gsde_native.cu)
+  if (a->stream == GSDE_STREAM_NATIVE &&
+      (a->pid_offset < 0 || a->pid_offset + a->n_particles > (1ll << 48)))
+    return set_error(GSDE_EINVAL, "ensemble: NATIVE stream particle ids must lie in [0, 2^48)");
   const bool native_inj = a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE;
   if (native_inj && o->occ)
     return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE does not sample the occupation "

@@ -22,12 +22,15 @@ struct gsde_graph_s {
   // native smem staging size for the whole graph (0 = too large, read via L2)
   int64_t nat_graph_smem = 0;
   // work-distribution counters of the native kernels: a ring of slots in the
-  // arena, one per call (zeroed stream-ordered before the launch), so up to
-  // kWorkSlots calls on one handle may be in flight on different streams
+  // arena, one per call (zeroed stream-ordered before the launch).  A slot is
+  // reused only after the kernel that last used it has finished: each launch
+  // records the slot's event, and the next user's stream waits on it before
+  // the memset (cheap: a slot comes round again only after kWorkSlots calls).
   static constexpr int kWorkSlots = 64;
   unsigned long long *work = nullptr;
+  cudaEvent_t work_done[kWorkSlots] = {};
   std::atomic<uint32_t> work_ticket{0};
-  unsigned long long *next_work_slot() { return work + (work_ticket++ % kWorkSlots); }
+  int next_work_slot() { return (int)(work_ticket++ % kWorkSlots); }
 };
 
 namespace gsde {

@@ -43,6 +43,10 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kMinBlocks = GSDE_MIN_BLOCKS;  // 4: caps registers at 64 -> 32 warps / SM
 constexpr int kMinBlocksStar = 3;            // star-graph ensembles: <= 85 registers
+#ifndef GSDE_MIN_BLOCKS_STAR_ZD
+#define GSDE_MIN_BLOCKS_STAR_ZD 3
+#endif
+constexpr int kMinBlocksStarZD = GSDE_MIN_BLOCKS_STAR_ZD;  // driftless star ensembles
 // trials: the compiler settles at 40 registers (48 warps / SM) under a 64-register
 // bound; the same kernel scheduled under a 51-register bound (5 blocks) ran 3% slower
 constexpr int kMinBlocksTrials = 4;
@@ -242,25 +246,35 @@ constexpr int kOccTabEdges = 1024;  // per-edge occupation records staged in sha
 // graph, occupation counters.
 struct Shared {
   int *priv;                 // [kPriv][kThreads]
-  int *mh;                   // [cap+1]
+  int *mh;                   // [cap+1], or null: bins >= kPriv go straight to mh_g
+  int64_t *mh_g;             // the call's M histogram (global)
   unsigned long long *tot;   // [4]
   int *exit_priv;            // trials: [E][kThreads] or null
   unsigned *occ;             // [n_cells] or null
 };
 
+// M-histogram bins kept in shared memory: any cap up to 8192 (32 KB); larger
+// caps (the reference accepts any) count bins >= kPriv with global atomics
+constexpr int kMaxSmemBins = 8192;
+__host__ __device__ __forceinline__ int smem_bins(int nb) { return nb <= kMaxSmemBins ? nb : 0; }
+
 __device__ __forceinline__ size_t shared_head_bytes(int nb) {
-  return align16((size_t)(kPriv * kThreads + nb) * sizeof(int)) + 4 * sizeof(unsigned long long);
+  return align16((size_t)(kPriv * kThreads + smem_bins(nb)) * sizeof(int)) +
+         4 * sizeof(unsigned long long);
 }
 
 template <bool STAR, bool SMEM>
-__device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, Shared &S,
-                                             Tables<SMEM> &T, bool exit_priv, int occ_cells) {
+__device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64_t *m_hist,
+                                             Shared &S, Tables<SMEM> &T, bool exit_priv,
+                                             int occ_cells) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int nbs = smem_bins(nb);
   S.priv = reinterpret_cast<int *>(smem);
-  S.mh = S.priv + kPriv * kThreads;
+  S.mh = nbs ? S.priv + kPriv * kThreads : nullptr;
+  S.mh_g = m_hist;
   S.tot = reinterpret_cast<unsigned long long *>(
-      smem + align16((size_t)(kPriv * kThreads + nb) * sizeof(int)));
-  for (int j = threadIdx.x; j < kPriv * kThreads + nb; j += blockDim.x) S.priv[j] = 0;
+      smem + align16((size_t)(kPriv * kThreads + nbs) * sizeof(int)));
+  for (int j = threadIdx.x; j < kPriv * kThreads + nbs; j += blockDim.x) S.priv[j] = 0;
   if (threadIdx.x < 4) S.tot[threadIdx.x] = 0ull;
   size_t off = shared_head_bytes(nb);
   T.edge = G.edge;
@@ -300,15 +314,18 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, Share
 __device__ __forceinline__ void mh_add(const Shared &S, int bin) {
   if (bin < kPriv)
     S.priv[bin * kThreads + threadIdx.x] += 1;
-  else
+  else if (S.mh)
     atomicAdd(&S.mh[bin], 1);
+  else if (S.mh_g)
+    add_i64(&S.mh_g[bin], 1);
 }
 
 __device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int occ_cells,
                              int64_t *occ_out) {
   __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    int64_t v = S.mh[b];
+  const int top = S.mh ? nb : (nb < kPriv ? nb : kPriv);
+  for (int b = threadIdx.x; b < top; b += blockDim.x) {
+    int64_t v = S.mh ? S.mh[b] : 0;
     if (b < kPriv)
       for (int t = 0; t < kThreads; ++t) v += S.priv[b * kThreads + t];
     if (v && m_hist) add_i64(&m_hist[b], v);
@@ -699,7 +716,8 @@ struct IterWords {
 // Star graphs: 3 blocks / SM (up to 85 registers, no spills, more ILP per
 // warp) measured +4% over 4 blocks / 64 registers; general graphs keep 4.
 template <class C, int Q, int SLOTS>
-__global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlocks)
+__global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD : kMinBlocksStar)
+                                                    : kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
                            unsigned long long *work, unsigned queue_off,
                            unsigned occ_tab_off, InjParams q) {
@@ -708,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM>(G, nb, S, T, false, C::OCC ? occ_smem_cells : 0);
+  shared_setup<C::STAR, C::SMEM>(G, nb, o.m_hist, S, T, false, C::OCC ? occ_smem_cells : 0);
   Occ O{o.hist_offsets, o.hist_counts, o.hist_dx, o.occ, S.occ, (int32_t)o.occ_every,
         (int32_t)o.occ_start, nullptr};
   if (C::OCC && G.n_edges <= kOccTabEdges) {
@@ -733,10 +751,16 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   L.M = 0;
   L.steps_left = 0;  // no particle in flight: every trip is a no-op
   L.occ_left = 1 << 30;
+  // Per-particle Philox block index: 32 bits in the counter's first word, and
+  // on wrap-around (2^32 blocks: >1e9 iterations of one particle) the carry
+  // goes to bits 48.. of the stream id word -- particle ids stay below 2^48
+  // (checked by the host), so streams never repeat, a run shorter than the
+  // wrap (every realistic one) is unaffected, and no extra register is live.
   uint32_t blk = 0;
+  static_assert((NB & (NB - 1)) == 0, "2^32 must be a multiple of the blocks per iteration");
   uint64_t id = 0;
   int64_t t_cross = 0, t_events = 0, t_truncs = 0, t_over = 0;
-  bool waiting = i < p.n;  // next particle not started yet
+  bool waiting = false;    // next particle not started yet
   bool active = false;     // a particle is in flight
   bool need = false;       // finished: fetch the next particle id
   bool queued = false;     // this lane's finished state awaits binning
@@ -751,16 +775,14 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     active = false;
     need = true;
   };
-  if (p.n_steps == 0) {  // placement only (engine.py:329-336)
-    while (waiting) {
-      id = (uint64_t)(p.id_offset + i);
-      place_native(L, G, T, O, p, q, id, star_len);
+  if (p.n_steps == 0) {  // placement only (engine.py:329-336): every particle once
+    for (; i < p.n; i += stride) {
+      place_native(L, G, T, O, p, q, (uint64_t)(p.id_offset + i), star_len);
       epilogue_particle(o, i, L.e, (double)L.x, 0, 0, 0);
       epilogue_bins(o, L.e, (double)L.x);
-      i += stride;
-      waiting = i < p.n;
     }
-    L.steps_left = 0;
+    shared_flush(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
+    return;
   }
 
   // Particles come from a grid-wide counter, 32 per warp refill, so warps the
@@ -882,6 +904,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
         trip<C, false>(L, G, T, S, O, p, z1, 0u);
     }
     blk += NB;
+    if (blk == 0u) id += 1ull << 48;
     if (active && L.steps_left == 0) finish();
   }
   if (bins && f_n > 0) flush_bins(f_n);
@@ -903,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM>(G, nb, S, T, exit_priv != 0, 0);
+  shared_setup<C::STAR, C::SMEM>(G, nb, o.m_hist, S, T, exit_priv != 0, 0);
   const Occ O{};
   const float inf = __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -912,7 +935,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   Lane<C> L;
   uint32_t pair = 0;
   uint64_t id = 0;
-  int32_t t_M = 0, t_ev = 0, t_tr = 0, t_over = 0;  // per lane: <= ~1e4 trials x cap
+  // per-lane sums; t_M (<= trials per lane x cap) spills to the global total
+  // before it could overflow
+  int32_t t_M = 0, t_ev = 0, t_tr = 0, t_over = 0;
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
     L.load_edge(T, O, C::STAR ? 0 : p.start_edge, p.sqdt, inf);
@@ -948,6 +973,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
       add_i64(&o.exit_counts[L.e], 1);
     mh_add(S, L.M > p.cap ? p.cap : L.M);
     t_M += L.M;
+    if (t_M >= (1 << 30)) {
+      if (o.totals) add_i64(&o.totals[0], t_M);
+      t_M = 0;
+    }
     t_ev += L.M > 0 ? 1 : 0;
     t_tr += L.trunc ? 1 : 0;
     i += stride;
@@ -1021,7 +1050,7 @@ __global__ void __launch_bounds__(256) histogram_kernel(int64_t n, const int64_t
 constexpr int kOccSmemCells = 8192;  // shared uint32 occupation counters up to 32 KB
 
 size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit, int occ_cells) {
-  size_t b = ((size_t)(kPriv * kThreads + nb) * sizeof(int) + 15) & ~size_t(15);
+  size_t b = ((size_t)(kPriv * kThreads + smem_bins(nb)) * sizeof(int) + 15) & ~size_t(15);
   b += 4 * sizeof(unsigned long long);
   if (stage) b += (size_t)g->E * (g->is_star ? 16 : 32) + (size_t)g->S * 16;
   if (priv_exit) b += (size_t)g->E * kThreads * sizeof(int);
@@ -1144,11 +1173,23 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     // grid-wide particle counter: this call's slot of the handle's ring
     // (a per-call cudaMallocAsync here stalled running kernels for up to
     // hundreds of ms when the pool remapped memory)
-    unsigned long long *work = const_cast<gsde_graph *>(g)->next_work_slot();
+    gsde_graph *gm = const_cast<gsde_graph *>(g);
+    const int slot = gm->next_work_slot();
+    unsigned long long *work = gm->work + slot;
+    cudaEvent_t &done = gm->work_done[slot];
+    if (!done) {
+      err = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      if (err != cudaSuccess) return err;
+    } else {  // the slot's previous kernel (maybe on another stream) must be finished
+      err = cudaStreamWaitEvent(s, done, 0);
+      if (err != cudaSuccess) return err;
+    }
     err = cudaMemsetAsync(work, 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
-    return launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
-                  (unsigned)(qoff + queues), q);
+    err = launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
+                 (unsigned)(qoff + queues), q);
+    if (err != cudaSuccess) return err;
+    return cudaEventRecord(done, s);
   };
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
                               inj)

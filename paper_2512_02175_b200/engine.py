@@ -333,18 +333,32 @@ def _chunk_bounds(n: int) -> np.ndarray:
     return bounds
 
 
-def _ensemble_to_host(graph, field, config):
+def _ensemble_to_host(graph, field, config, pid_offset=0, n_particles=None, grid=None,
+                      edge_counts=False, estimators=False):
     """run_ensemble's device work + transfers: per-particle arrays land in
     pinned host memory; large runs are split by global particle id (results
     are identical: every particle's stream is keyed by its id, the fused
-    counts are integer sums) so transfers overlap the next chunk's kernel."""
+    counts are integer sums) so transfers overlap the next chunk's kernel.
+
+    ``pid_offset`` / ``n_particles`` select a shard of global ids (multi-GPU
+    ranks).  With ``estimators=True`` returns ``(host arrays, device
+    estimators)`` -- the chunks' fused estimators summed on the device (M
+    histogram, totals, and ``edge_counts`` / the ``grid`` histogram when
+    asked) -- instead of the flat list."""
     import torch
 
     names = ("edge", "x", "crossings", "events")
-    n = config.n_particles
+    n = config.n_particles if n_particles is None else int(n_particles)
+    outs = names + (("edge_counts",) if edge_counts else ())
+    est_keys = ("m_hist", "totals") + (("edge_counts",) if edge_counts else ()) + (
+        ("hist",) if grid is not None else ())
     if n < _PIPELINE_MIN:
-        res = ensemble_device(graph, field, config, outputs=names)
-        return _to_host([res[k] for k in names + ("m_hist", "totals")])
+        res = ensemble_device(graph, field, config, pid_offset=pid_offset, n_particles=n,
+                              outputs=outs, grid=grid)
+        if not estimators:
+            return _to_host([res[k] for k in names + ("m_hist", "totals")])
+        hosts = _to_host([res[k] for k in names])
+        return hosts, {k: res[k] for k in est_keys}
     _, dev = _native.torch_cuda(config.device)
     compute = torch.cuda.current_stream(dev)
     streams = _COPY_STREAMS.get(dev)
@@ -363,8 +377,9 @@ def _ensemble_to_host(graph, field, config):
         # SMs its predecessor's tail leaves idle (separate outputs; integer sums)
         st = compute if c % 2 == 0 else side
         with torch.cuda.stream(st):
-            res = ensemble_device(graph, field, config, pid_offset=int(lo),
-                                  n_particles=int(hi - lo), outputs=names, stream=st.cuda_stream)
+            res = ensemble_device(graph, field, config, pid_offset=int(pid_offset + lo),
+                                  n_particles=int(hi - lo), outputs=outs, grid=grid,
+                                  stream=st.cuda_stream)
         done = torch.cuda.Event()
         done.record(st)
         copier.wait_event(done)
@@ -374,9 +389,11 @@ def _ensemble_to_host(graph, field, config):
         parts.append(res)  # keeps the device buffers alive until the copies finished
     copier.synchronize()
     compute.wait_stream(side)
-    m_hist = sum(r["m_hist"] for r in parts).cpu().numpy()
-    totals = sum(r["totals"] for r in parts).cpu().numpy()
-    return [h.numpy() for h in hosts] + [m_hist, totals]
+    est = {k: sum(r[k] for r in parts) for k in est_keys}
+    if estimators:
+        return [h.numpy() for h in hosts], est
+    return [h.numpy() for h in hosts] + [est["m_hist"].cpu().numpy(),
+                                         est["totals"].cpu().numpy()]
 
 
 def _multi_device(graph, field, config):

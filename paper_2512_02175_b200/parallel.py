@@ -59,24 +59,38 @@ class DistributedResult:
     histogram: np.ndarray | None
     n_particles: int
     shard: tuple
+    #: this rank's shard of the per-particle arrays (host numpy, reference
+    #: dtypes) when asked for with ``particles=True``: edges, positions,
+    #: crossings, crossing_events of global ids shard[0] .. shard[0]+shard[1]-1
+    particles: dict | None = None
 
 
 def run_ensemble_distributed(graph, field, config, grid=None, group=None,
-                             edge_counts: bool = True) -> DistributedResult:
+                             edge_counts: bool = True,
+                             particles: bool = False) -> DistributedResult:
     """Run ``config.n_particles`` particles sharded over the ranks of the
     default process group (one GPU per rank), estimators merged with one
-    NCCL all-reduce.  Per-particle arrays stay on each rank's GPU."""
+    NCCL all-reduce.  Per-particle arrays stay on each rank's GPU unless
+    ``particles=True``: then each rank copies its shard to (pinned) host
+    memory through ``run_ensemble``'s chunked transfer pipeline -- the
+    distributed form of ``run_ensemble``'s result."""
     import torch.distributed as dist
 
-    from .engine import _check_ensemble_shape, ensemble_device
+    from .engine import _check_ensemble_shape, _ensemble_to_host, ensemble_device
 
     config = config.validated(graph)
     _check_ensemble_shape(graph, config)
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     off, cnt = shard_range(config.n_particles, rank, world)
-    res = ensemble_device(graph, field, config, pid_offset=off, n_particles=cnt,
-                          outputs=("edge_counts",) if edge_counts else (), grid=grid)
+    host = None
+    if particles:
+        arrs, res = _ensemble_to_host(graph, field, config, pid_offset=off, n_particles=cnt,
+                                      grid=grid, edge_counts=edge_counts, estimators=True)
+        host = dict(zip(("edges", "positions", "crossings", "crossing_events"), arrs))
+    else:
+        res = ensemble_device(graph, field, config, pid_offset=off, n_particles=cnt,
+                              outputs=("edge_counts",) if edge_counts else (), grid=grid)
     merged = merge_estimators(res, group)
     tot = merged["totals"].cpu().numpy()
     return DistributedResult(
@@ -88,6 +102,7 @@ def run_ensemble_distributed(graph, field, config, grid=None, group=None,
         histogram=merged["hist"].cpu().numpy() if "hist" in merged else None,
         n_particles=config.n_particles,
         shard=(off, cnt),
+        particles=host,
     )
 
 

@@ -8,7 +8,12 @@
                    Poiseuille flux, drift from_flux, emitted through the graph-file
                    format so every consumer loads the identical graph.
 
-All generators are deterministic functions of their arguments.
+All generators are deterministic functions of their arguments.  Each takes an
+optional ``api`` -- a module exposing the reference's graph-construction names
+(``build_graph``, ``CoefficientField``, ``ConstantDrift``, ``LinearDrift`` and a
+``graphfile`` submodule): this package by default, or the reference ``graphsde``
+itself, so ``bench.py``'s reference arm times the reference on the identical
+graphs.
 """
 
 from __future__ import annotations
@@ -17,36 +22,47 @@ import math
 
 import numpy as np
 
-from .coefficients import CoefficientField, ConstantDrift, LinearDrift
-from .graph import build_graph
-from .graphfile import network_tables_to_graph_file, parse_graph_file
+import importlib
+import sys
 
 
-def star(n_edges: int, drift, sigma=1.0, weights=None):
-    graph = build_graph([(0, None, math.inf)] * n_edges, {0: weights} if weights else None)
+def _api(api):
+    return sys.modules[__package__] if api is None else api
+
+
+def _graphfile(api):
+    return importlib.import_module(_api(api).__name__ + ".graphfile")
+
+
+def star(n_edges: int, drift, sigma=1.0, weights=None, api=None):
+    A = _api(api)
+    graph = A.build_graph([(0, None, math.inf)] * n_edges, {0: weights} if weights else None)
     drift = list(drift)
     sig = [sigma] * n_edges if np.isscalar(sigma) else list(sigma)
-    return graph, CoefficientField.for_graph(graph, drift, sig)
+    return graph, A.CoefficientField.for_graph(graph, drift, sig)
 
 
-def star3():
-    return star(3, [ConstantDrift(0.0)] * 3)
+def star3(api=None):
+    return star(3, [_api(api).ConstantDrift(0.0)] * 3, api=api)
 
 
-def star5(kind: str = "linear"):
+def star5(kind: str = "linear", api=None):
+    A = _api(api)
     if kind == "linear":
-        drift = [ConstantDrift(-10.0 * i) for i in range(1, 6)]
+        drift = [A.ConstantDrift(-10.0 * i) for i in range(1, 6)]
     else:
-        drift = [LinearDrift(-10.0 * i) for i in range(1, 6)]
-    return star(5, drift)
+        drift = [A.LinearDrift(-10.0 * i) for i in range(1, 6)]
+    return star(5, drift, api=api)
 
 
-def hub64(seed: int = 0):
+def hub64(seed: int = 0, api=None):
+    A = _api(api)
     rng = np.random.default_rng(seed)
     lengths = rng.uniform(0.5, 2.0, 64)
     ks = rng.uniform(1.0, 20.0, 64)
-    graph = build_graph([(0, i + 1, float(lengths[i])) for i in range(64)])
-    field = CoefficientField.for_graph(graph, [LinearDrift(-float(k)) for k in ks], [1.0] * 64)
+    graph = A.build_graph([(0, i + 1, float(lengths[i])) for i in range(64)])
+    field = A.CoefficientField.for_graph(graph, [A.LinearDrift(-float(k)) for k in ks],
+                                         [1.0] * 64)
     return graph, field
 
 
@@ -107,9 +123,9 @@ def vascular_tables(n_nodes: int = 100_000, seed: int = 2512, loop_frac: float =
     return nodes, segs
 
 
-def vascular_text(n_nodes: int = 100_000, seed: int = 2512) -> str:
-    return network_tables_to_graph_file(*vascular_tables(n_nodes, seed))
+def vascular_text(n_nodes: int = 100_000, seed: int = 2512, api=None) -> str:
+    return _graphfile(api).network_tables_to_graph_file(*vascular_tables(n_nodes, seed))
 
 
-def vascular(n_nodes: int = 100_000, seed: int = 2512):
-    return parse_graph_file(vascular_text(n_nodes, seed))
+def vascular(n_nodes: int = 100_000, seed: int = 2512, api=None):
+    return _graphfile(api).parse_graph_file(vascular_text(n_nodes, seed, api))

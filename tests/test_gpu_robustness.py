@@ -1,0 +1,93 @@
+"""GPU robustness edges of the native kernels:
+
+* ``n_steps == 0`` (placement only) counts every particle exactly once in the
+  fused histogram / edge counts;
+* caps whose M histogram exceeds the shared-memory bins (the reference accepts
+  any ``max_splits_per_step``) run, and agree with a small cap when no step
+  reaches it;
+* more in-flight launches on one graph handle than its work-counter ring has
+  slots, alternating between streams, equal serial launches;
+* particle ids beyond the native stream's 2^48 range are refused.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import _native, analysis, engine
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("rng", ["native", "reference"])
+@pytest.mark.parametrize("case", ["star3_bm", "hub64"])
+def test_placement_only_counts_each_particle_once(case, rng):
+    g, f = cases.build(case, gs)
+    grid = gs.EdgeGrid.uniform(g, 5, lengths=[2.0] * g.n_edges if g.is_star else None)
+    init = gs.PointStart(1, 0.3) if g.is_star else gs.PerEdgeUniform(2.0)
+    n = 100_003
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=0, n_particles=n, seed=4, initial=init, rng=rng)
+    res = engine.ensemble_device(g, f, cfg, outputs=("all", "edge_counts"), grid=grid)
+    assert int(res["hist"].sum()) == n
+    assert int(res["edge_counts"].sum()) == n
+    ec = np.bincount(res["edge"].cpu().numpy(), minlength=g.n_edges)
+    np.testing.assert_array_equal(res["edge_counts"].cpu().numpy(), ec)
+    h, _ = analysis.run_ensemble_histogram(g, f, cfg, grid)
+    assert h.counts.sum() == n
+    np.testing.assert_array_equal(h.counts, res["hist"].cpu().numpy())
+
+
+@pytest.mark.parametrize("case", ["star5_linear", "hub64"])
+def test_cap_beyond_shared_bins(case):
+    """cap = 20000 -> 20001 M bins (> the 8192 kept in shared memory): bins >= 8
+    go to global atomics.  No step here reaches M = 100, so a cap-100 run of
+    the same streams must give the same M histogram and outputs."""
+    g, f = cases.build(case, gs)
+    init = gs.AtVertex(0) if g.is_star else gs.PerEdgeUniform(2.0)
+    mk = lambda cap: gs.SimulationConfig(dt=1e-2, n_steps=200, n_particles=200_000, seed=8,
+                                         initial=init, max_splits_per_step=cap)
+    big = engine.ensemble_device(g, f, mk(20_000))
+    small = engine.ensemble_device(g, f, mk(100))
+    mb, ms = big["m_hist"].cpu().numpy(), small["m_hist"].cpu().numpy()
+    assert mb[101:].sum() == 0 and mb.size == 20_001
+    np.testing.assert_array_equal(mb[:101], ms)
+    for k in ("edge", "x", "crossings", "events"):
+        assert torch.equal(big[k], small[k]), k
+    tb = engine.trials_device(g, f, 1e-2, 300_000, 3, max_splits=20_000, per_trial=False)
+    ts = engine.trials_device(g, f, 1e-2, 300_000, 3, max_splits=100, per_trial=False)
+    np.testing.assert_array_equal(tb["m_hist"].cpu().numpy()[:101], ts["m_hist"].cpu().numpy())
+    assert torch.equal(tb["exit_counts"], ts["exit_counts"])
+
+
+def test_more_launches_in_flight_than_work_slots():
+    """80 native launches on one handle (ring of 64 work counters), queued on
+    two streams without host synchronisation: each equals its serial run."""
+    g, f = cases.build("hub8", gs)
+    cfgs = [gs.SimulationConfig(dt=1e-2, n_steps=50, n_particles=20_000 + 37 * i, seed=i,
+                                initial=gs.PerEdgeUniform(2.0)) for i in range(80)]
+    serial = []
+    for c in cfgs:
+        r = engine.ensemble_device(g, f, c, outputs=("edge", "crossings"))
+        torch.cuda.synchronize()
+        serial.append(r)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    queued = []
+    for i, c in enumerate(cfgs):
+        st = streams[i % 2]
+        with torch.cuda.stream(st):
+            queued.append(engine.ensemble_device(g, f, c, outputs=("edge", "crossings"),
+                                                 stream=st.cuda_stream))
+    torch.cuda.synchronize()
+    for a, b in zip(serial, queued):
+        for k in ("edge", "crossings", "m_hist", "totals"):
+            assert torch.equal(a[k], b[k]), k
+
+
+def test_native_particle_ids_below_2_48():
+    g, f = cases.build("star3_bm", gs)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=1, n_particles=10, seed=1)
+    engine.ensemble_device(g, f, cfg, pid_offset=(1 << 48) - 10)  # the last ten ids: fine
+    with pytest.raises(_native.GsdeError):
+        engine.ensemble_device(g, f, cfg, pid_offset=(1 << 48) - 9)
