@@ -263,6 +263,9 @@ void gsde_parsed_free(gsde_parsed *p);
 uint64_t gsde_raw64(uint64_t seed, uint64_t stream, uint64_t index); /* rng.py:45-66 */
 double gsde_uniform01(uint64_t seed, uint64_t stream, uint64_t index); /* rng.py:75-78 */
 double gsde_normal(uint64_t seed, uint64_t stream, uint64_t index);    /* rng.py:146-149 */
+double gsde_u64_to_uniform(uint64_t r);                                /* rng.py:69-72 */
+double gsde_u64_to_normal(uint64_t r);                                 /* rng.py:137-143 */
+double gsde_norm_ppf(double p);                                        /* rng.py:81-134 */
 double gsde_solve_first_passage_s(double a, double b, double c);     /* kernels.py:88-131 */
 
 /* Number of kernels this library has launched (instrumentation for bench.py). */

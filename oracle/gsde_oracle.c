@@ -131,8 +131,10 @@ double orc_norm_ppf(double p) {
 double orc_u64_to_normal(uint64_t r) {
   int64_t n = (int64_t)(r >> 11);
   double q = ((double)(n - 4503599627370496LL) + 0.5) * INV_2_53;
+  /* upper half: 1 - p as the reference's compiled (fastmath) code forms it,
+   * 1 - n 2^-53 (the 2^-54 term is reassociated away; tests/golden/validators.json) */
   double pt = q < 0.0 ? ((double)n + 0.5) * INV_2_53
-                      : ((double)(9007199254740992LL - n) - 0.5) * INV_2_53;
+                      : (double)(9007199254740992LL - n) * INV_2_53;
   return norm_ppf_qt(q, pt);
 }
 

@@ -99,7 +99,8 @@ EXPORTS = (
     "gsde_vertex_trials", "gsde_step_batch", "gsde_histogram", "gsde_raw64", "gsde_uniform01",
     "gsde_normal", "gsde_solve_first_passage_s", "gsde_launch_count", "gsde_abi_version",
     "gsde_last_error", "gsde_parse_graph_text", "gsde_parsed_sizes", "gsde_parsed_export",
-    "gsde_parsed_free", "gsde_fvm_run",
+    "gsde_parsed_free", "gsde_fvm_run", "gsde_u64_to_uniform", "gsde_u64_to_normal",
+    "gsde_norm_ppf",
 )
 
 _lib = None
@@ -132,6 +133,11 @@ def lib():
                 for name in ("gsde_uniform01", "gsde_normal"):
                     getattr(L, name).argtypes = [_u64, _u64, _u64]
                     getattr(L, name).restype = _f64
+                for name in ("gsde_u64_to_uniform", "gsde_u64_to_normal"):
+                    getattr(L, name).argtypes = [_u64]
+                    getattr(L, name).restype = _f64
+                L.gsde_norm_ppf.argtypes = [_f64]
+                L.gsde_norm_ppf.restype = _f64
                 L.gsde_solve_first_passage_s.argtypes = [_f64, _f64, _f64]
                 L.gsde_solve_first_passage_s.restype = _f64
                 L.gsde_parse_graph_text.argtypes = [C.c_char_p, _i64, C.POINTER(_P)]

@@ -158,6 +158,12 @@ double gsde_uniform01(uint64_t seed, uint64_t stream, uint64_t index) {
 double gsde_normal(uint64_t seed, uint64_t stream, uint64_t index) {
   return u64_to_normal(raw64(seed, stream, index));
 }
+double gsde_u64_to_uniform(uint64_t r) { return u53_to_uniform(r >> 11); }
+double gsde_u64_to_normal(uint64_t r) { return u64_to_normal(r); }
+double gsde_norm_ppf(double p) {
+  const double q = p - 0.5;
+  return norm_ppf_qt(q, q < 0.0 ? p : 1.0 - p);
+}
 double gsde_solve_first_passage_s(double a, double b, double c) {
   return solve_first_passage_s<double>(a, b, c);
 }

@@ -125,12 +125,19 @@ GSDE_HD double norm_ppf_qt(double q, double pt) {
   return q < 0.0 ? x : -x;
 }
 
-// rng.py:137-143: p = (n + 1/2) 2^-53; q and min(p, 1-p) formed exactly.
+// rng.py:137-143: p = (n + 1/2) 2^-53 on the 53-bit lattice n = r >> 11.
+// q = p - 1/2 is formed exactly; the tail probability min(p, 1 - p) is what
+// the reference's COMPILED code computes (numba fastmath, kernels and rng
+// alike): p itself below 1/2, and 1 - n 2^-53 above -- LLVM reassociates
+// 1 - (n + 1/2) 2^-53 into (1 - 2^-54) - n 2^-53 and 1 - 2^-54 rounds to 1,
+// so the upper tail sits half a lattice step from the lower one (pinned by
+// tests/golden/validators.json: the top lattice points give 8.2095, 8.1259,
+// 8.0766, ... exactly as graphsde.rng.u64_to_normal).
 GSDE_HD double u64_to_normal(uint64_t r) {
   const int64_t n = (int64_t)(r >> 11);
   const double q = ((double)(n - 4503599627370496LL) + 0.5) * kInv2p53;
   const double pt = q < 0.0 ? ((double)n + 0.5) * kInv2p53
-                            : ((double)(9007199254740992LL - n) - 0.5) * kInv2p53;
+                            : (double)(9007199254740992LL - n) * kInv2p53;
   return norm_ppf_qt(q, pt);
 }
 

@@ -29,6 +29,7 @@
 //    histogram in the particle epilogue.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
@@ -43,10 +44,6 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kMinBlocks = GSDE_MIN_BLOCKS;  // 4: caps registers at 64 -> 32 warps / SM
 constexpr int kMinBlocksStar = 3;            // star-graph ensembles: <= 85 registers
-#ifndef GSDE_MIN_BLOCKS_STAR_ZD
-#define GSDE_MIN_BLOCKS_STAR_ZD 3
-#endif
-constexpr int kMinBlocksStarZD = GSDE_MIN_BLOCKS_STAR_ZD;  // driftless star ensembles
 // trials: the compiler settles at 40 registers (48 warps / SM) under a 64-register
 // bound; the same kernel scheduled under a 51-register bound (5 blocks) ran 3% slower
 constexpr int kMinBlocksTrials = 4;
@@ -200,7 +197,7 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 
 // Compile-time kernel variant.
 template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false,
-          bool INJ_ = false>
+          bool INJ_ = false, bool WIDE_ = false>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
@@ -211,6 +208,12 @@ struct Cfg {
   // parity mode: the production kernel fed the reference's injected draws
   // (one per use, in the reference's order) and its inverse-CDF exit slots
   static constexpr bool INJ = INJ_;
+  // long / high-cap runs (chosen by the host only when a 32-bit per-lane
+  // count, the shared M-histogram or the 32-bit Philox block index could
+  // overflow): int64 per-particle counters, M bins beyond kMaxSmemBins in
+  // global memory, 64-bit block index.  Common runs keep the 32-bit kernel.
+  static constexpr bool WIDE = WIDE_;
+  using Cnt = std::conditional_t<WIDE_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
 };
 
@@ -246,37 +249,45 @@ constexpr int kOccTabEdges = 1024;  // per-edge occupation records staged in sha
 // graph, occupation counters.
 struct Shared {
   int *priv;                 // [kPriv][kThreads]
-  int *mh;                   // [cap+1], or null: bins >= kPriv go straight to mh_g
-  int64_t *mh_g;             // the call's M histogram (global)
+  int *mh;                   // [min(cap+1, kMaxSmemBins)]
+  int nbs;                   // M bins in shared memory (WIDE kernels: the rest in mh_g)
+  int64_t *mh_g;             // the call's M histogram (global; WIDE kernels)
   unsigned long long *tot;   // [4]
   int *exit_priv;            // trials: [E][kThreads] or null
   unsigned *occ;             // [n_cells] or null
 };
 
-// M-histogram bins kept in shared memory: any cap up to 8192 (32 KB); larger
-// caps (the reference accepts any) count bins >= kPriv with global atomics
+// M-histogram bins kept in shared memory: caps up to 8191 (32 KB); a larger
+// cap (the reference accepts any) selects a WIDE kernel, which counts the
+// bins beyond in global memory
 constexpr int kMaxSmemBins = 8192;
-__host__ __device__ __forceinline__ int smem_bins(int nb) { return nb <= kMaxSmemBins ? nb : 0; }
-
-__device__ __forceinline__ size_t shared_head_bytes(int nb) {
-  return align16((size_t)(kPriv * kThreads + smem_bins(nb)) * sizeof(int)) +
-         4 * sizeof(unsigned long long);
+__host__ __device__ __forceinline__ int smem_bins(int nb) {
+  return nb < kMaxSmemBins ? nb : kMaxSmemBins;
 }
 
-template <bool STAR, bool SMEM>
+__device__ __forceinline__ size_t shared_head_bytes(int nbs) {
+  return align16((size_t)(kPriv * kThreads + nbs) * sizeof(int)) + 4 * sizeof(unsigned long long);
+}
+
+// (WIDE: the shared M bins are capped at kMaxSmemBins; otherwise the host
+// guarantees cap + 1 <= kMaxSmemBins)
+template <bool STAR, bool SMEM, bool WIDE = false>
 __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64_t *m_hist,
                                              Shared &S, Tables<SMEM> &T, bool exit_priv,
                                              int occ_cells) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int nbs = smem_bins(nb);
+  const int nbs = WIDE ? smem_bins(nb) : nb;
   S.priv = reinterpret_cast<int *>(smem);
-  S.mh = nbs ? S.priv + kPriv * kThreads : nullptr;
-  S.mh_g = m_hist;
+  S.mh = S.priv + kPriv * kThreads;
+  if (WIDE) {
+    S.nbs = nbs;
+    S.mh_g = m_hist;
+  }
   S.tot = reinterpret_cast<unsigned long long *>(
       smem + align16((size_t)(kPriv * kThreads + nbs) * sizeof(int)));
   for (int j = threadIdx.x; j < kPriv * kThreads + nbs; j += blockDim.x) S.priv[j] = 0;
   if (threadIdx.x < 4) S.tot[threadIdx.x] = 0ull;
-  size_t off = shared_head_bytes(nb);
+  size_t off = shared_head_bytes(nbs);
   T.edge = G.edge;
   T.edgev = G.edgev;
   T.col = G.col;
@@ -311,21 +322,23 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64
   __syncthreads();
 }
 
+template <bool WIDE>
 __device__ __forceinline__ void mh_add(const Shared &S, int bin) {
   if (bin < kPriv)
     S.priv[bin * kThreads + threadIdx.x] += 1;
-  else if (S.mh)
+  else if (!WIDE || bin < S.nbs)
     atomicAdd(&S.mh[bin], 1);
   else if (S.mh_g)
     add_i64(&S.mh_g[bin], 1);
 }
 
+template <bool WIDE = false>
 __device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int occ_cells,
                              int64_t *occ_out) {
   __syncthreads();
-  const int top = S.mh ? nb : (nb < kPriv ? nb : kPriv);
-  for (int b = threadIdx.x; b < top; b += blockDim.x) {
-    int64_t v = S.mh ? S.mh[b] : 0;
+  const int nbs = WIDE ? smem_bins(nb) : nb;
+  for (int b = threadIdx.x; b < nbs; b += blockDim.x) {
+    int64_t v = S.mh[b];
     if (b < kPriv)
       for (int t = 0; t < kThreads; ++t) v += S.priv[b * kThreads + t];
     if (v && m_hist) add_i64(&m_hist[b], v);
@@ -350,7 +363,7 @@ struct Lane {
   float len;       // edge length (star: mirror wall or +inf)
   int4 ev;         // endpoint alias info of e (general graphs)
   int steps_left;
-  int cross, events, truncs;
+  typename C::Cnt cross, events, truncs;
   int occ_left;    // steps to the next occupation sample
   // Cfg::INJ only: the reference's slot tables, this particle's injected
   // draws and the next draw index
@@ -431,7 +444,7 @@ struct Lane {
       cross += M;
       events += 1;
       truncs += trunc ? 1 : 0;
-      mh_add(S, M > cap ? cap : M);
+      mh_add<C::WIDE>(S, M > cap ? cap : M);
     }
     M = 0;
     trunc = false;
@@ -716,8 +729,7 @@ struct IterWords {
 // Star graphs: 3 blocks / SM (up to 85 registers, no spills, more ILP per
 // warp) measured +4% over 4 blocks / 64 registers; general graphs keep 4.
 template <class C, int Q, int SLOTS>
-__global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD : kMinBlocksStar)
-                                                    : kMinBlocks)
+__global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlocks)
     native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
                            unsigned long long *work, unsigned queue_off,
                            unsigned occ_tab_off, InjParams q) {
@@ -726,7 +738,8 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD 
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM>(G, nb, o.m_hist, S, T, false, C::OCC ? occ_smem_cells : 0);
+  shared_setup<C::STAR, C::SMEM, C::WIDE>(G, nb, o.m_hist, S, T, false,
+                                          C::OCC ? occ_smem_cells : 0);
   Occ O{o.hist_offsets, o.hist_counts, o.hist_dx, o.occ, S.occ, (int32_t)o.occ_every,
         (int32_t)o.occ_start, nullptr};
   if (C::OCC && G.n_edges <= kOccTabEdges) {
@@ -751,16 +764,15 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD 
   L.M = 0;
   L.steps_left = 0;  // no particle in flight: every trip is a no-op
   L.occ_left = 1 << 30;
-  // Per-particle Philox block index: 32 bits in the counter's first word, and
-  // on wrap-around (2^32 blocks: >1e9 iterations of one particle) the carry
-  // goes to bits 48.. of the stream id word -- particle ids stay below 2^48
-  // (checked by the host), so streams never repeat, a run shorter than the
-  // wrap (every realistic one) is unaffected, and no extra register is live.
+  // Per-particle Philox block index: 32 bits in the counter's first word.
+  // WIDE kernels (runs that could pass 2^32 blocks per particle) carry the
+  // wrap into bits 48.. of the stream-id word -- particle ids stay below 2^48
+  // (checked by the host) -- so streams never repeat.
   uint32_t blk = 0;
   static_assert((NB & (NB - 1)) == 0, "2^32 must be a multiple of the blocks per iteration");
   uint64_t id = 0;
   int64_t t_cross = 0, t_events = 0, t_truncs = 0, t_over = 0;
-  bool waiting = false;    // next particle not started yet
+  bool waiting = i < p.n;  // next particle not started yet
   bool active = false;     // a particle is in flight
   bool need = false;       // finished: fetch the next particle id
   bool queued = false;     // this lane's finished state awaits binning
@@ -775,14 +787,20 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD 
     active = false;
     need = true;
   };
-  if (p.n_steps == 0) {  // placement only (engine.py:329-336): every particle once
-    for (; i < p.n; i += stride) {
-      place_native(L, G, T, O, p, q, (uint64_t)(p.id_offset + i), star_len);
+
+  // Placement only (engine.py:329-336): every particle placed and binned once
+  // here; the host starts the particle counter past every id (launch below),
+  // so the hand-out loop that follows starts nothing.
+  if (p.n_steps == 0) {
+    while (waiting) {
+      id = (uint64_t)(p.id_offset + i);
+      place_native(L, G, T, O, p, q, id, star_len);
       epilogue_particle(o, i, L.e, (double)L.x, 0, 0, 0);
       epilogue_bins(o, L.e, (double)L.x);
+      i += stride;
+      waiting = i < p.n;
     }
-    shared_flush(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
-    return;
+    L.steps_left = 0;
   }
 
   // Particles come from a grid-wide counter, 32 per warp refill, so warps the
@@ -904,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD 
         trip<C, false>(L, G, T, S, O, p, z1, 0u);
     }
     blk += NB;
-    if (blk == 0u) id += 1ull << 48;
+    if (C::WIDE && blk == 0u) id += 1ull << 48;
     if (active && L.steps_left == 0) finish();
   }
   if (bins && f_n > 0) flush_bins(f_n);
@@ -914,7 +932,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? (C::ZD ? kMinBlocksStarZD 
     warp_add_i64(&o.totals[2], t_truncs);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
+  shared_flush<C::WIDE>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
 }
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
@@ -926,7 +944,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM>(G, nb, o.m_hist, S, T, exit_priv != 0, 0);
+  shared_setup<C::STAR, C::SMEM, C::WIDE>(G, nb, o.m_hist, S, T, exit_priv != 0, 0);
   const Occ O{};
   const float inf = __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -935,9 +953,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   Lane<C> L;
   uint32_t pair = 0;
   uint64_t id = 0;
-  // per-lane sums; t_M (<= trials per lane x cap) spills to the global total
-  // before it could overflow
-  int32_t t_M = 0, t_ev = 0, t_tr = 0, t_over = 0;
+  // per-lane sums: trials per lane x cap < 2^31 unless the host chose WIDE
+  typename C::Cnt t_M = 0;
+  int32_t t_ev = 0, t_tr = 0, t_over = 0;
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
     L.load_edge(T, O, C::STAR ? 0 : p.start_edge, p.sqdt, inf);
@@ -971,12 +989,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
       S.exit_priv[L.e * kThreads + threadIdx.x] += 1;
     else if (o.exit_counts)
       add_i64(&o.exit_counts[L.e], 1);
-    mh_add(S, L.M > p.cap ? p.cap : L.M);
+    mh_add<C::WIDE>(S, L.M > p.cap ? p.cap : L.M);
     t_M += L.M;
-    if (t_M >= (1 << 30)) {
-      if (o.totals) add_i64(&o.totals[0], t_M);
-      t_M = 0;
-    }
     t_ev += L.M > 0 ? 1 : 0;
     t_tr += L.trunc ? 1 : 0;
     i += stride;
@@ -1009,7 +1023,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     warp_add_i64(&o.totals[2], t_tr);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush(S, nb, o.m_hist, 0, nullptr);
+  shared_flush<C::WIDE>(S, nb, o.m_hist, 0, nullptr);
   if (S.exit_priv && o.exit_counts) {
     for (int e = threadIdx.x; e < G.n_edges; e += blockDim.x) {
       int64_t v = 0;
@@ -1100,20 +1114,26 @@ cudaError_t prepare(K kernel, size_t smem) {
 // Runtime flags -> compile-time kernel variant (Cfg).
 template <bool OCC, class F>
 cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
-                     bool inj = false) {
+                     bool inj = false, bool wide = false) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
     constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
     auto drift = [&](auto rf) -> cudaError_t {
       constexpr bool RF = decltype(rf)::value;
-      if (inj) {  // parity mode: no occupation sampling
+      if (inj) {  // parity mode: no occupation sampling, 32-bit counts
         if constexpr (!OCC) {
+          if (wide) return cudaErrorInvalidValue;
           if (tab) return f(Cfg<ST, SM, true, RF, false, false, true>{});
           return zd ? f(Cfg<ST, SM, false, RF, false, true, true>{})
                     : f(Cfg<ST, SM, false, RF, false, false, true>{});
         }
         return cudaErrorInvalidValue;
+      }
+      if (wide) {
+        if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, true>{});
+        return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, true>{})
+                  : f(Cfg<ST, SM, false, RF, OCC, false, false, true>{});
       }
       if (tab) return f(Cfg<ST, SM, true, RF, OCC>{});
       return zd ? f(Cfg<ST, SM, false, RF, OCC, true>{}) : f(Cfg<ST, SM, false, RF, OCC>{});
@@ -1124,6 +1144,15 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
   };
   if (star) return smem ? with(T{}, T{}) : with(T{}, N{});
   return smem ? with(N{}, T{}) : with(N{}, N{});
+}
+
+// Ensembles whose 32-bit per-lane counts, shared M histogram or Philox block
+// index could overflow take the WIDE kernel: per particle at most n_steps x
+// cap crossings, and at most (cap + 2) iterations (4 blocks each) per step.
+bool ensemble_needs_wide(const gsde_run &a) {
+  const double steps = (double)a.n_steps, cap = (double)a.cap;
+  return a.cap + 1 > kMaxSmemBins || steps * cap >= 2147483647.0 ||
+         4.0 * steps * (cap + 2.0) >= 4294967296.0;
 }
 
 }  // namespace
@@ -1172,29 +1201,31 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     smem = qoff + queues + occ_tab;
     // grid-wide particle counter: this call's slot of the handle's ring
     // (a per-call cudaMallocAsync here stalled running kernels for up to
-    // hundreds of ms when the pool remapped memory)
+    // hundreds of ms when the pool remapped memory).  A slot is reused only
+    // after the kernel that last used it finished (its event), so any number
+    // of calls may be in flight on any streams.
     gsde_graph *gm = const_cast<gsde_graph *>(g);
     const int slot = gm->next_work_slot();
     unsigned long long *work = gm->work + slot;
     cudaEvent_t &done = gm->work_done[slot];
-    if (!done) {
+    if (!done)
       err = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-      if (err != cudaSuccess) return err;
-    } else {  // the slot's previous kernel (maybe on another stream) must be finished
+    else
       err = cudaStreamWaitEvent(s, done, 0);
-      if (err != cudaSuccess) return err;
-    }
-    err = cudaMemsetAsync(work, 0, sizeof(*work), s);
+    if (err != cudaSuccess) return err;
+    // (placement-only runs: 0x7f7f... -- past every particle id, nothing handed out)
+    err = cudaMemsetAsync(work, a.n_steps == 0 ? 0x7f : 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
     err = launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
                  (unsigned)(qoff + queues), q);
     if (err != cudaSuccess) return err;
     return cudaEventRecord(done, s);
   };
+  const bool wide = ensemble_needs_wide(a);
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
-                              inj)
+                              inj, wide)
              : dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                               run, inj);
+                               run, inj, wide);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
@@ -1210,9 +1241,13 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   const bool inj = a.stream == GSDE_STREAM_INJECT;  // (precision GSDE_PREC_NATIVE)
   const InjParams q{a.inj_raw,        a.inj_normal,       a.inj_stride,
                     g->ref32.v_thresh, g->ref32.v_edges, g->ref32.v_orient};
+  const bool out = o.M || o.edge || o.x || o.trunc;
+  // WIDE when a lane's sum of M (<= its trials x cap; conservatively one
+  // block per SM) could pass 2^31 or the M histogram outgrows shared memory
+  const double per_lane = std::ceil((double)n / ((double)dev_info(d).sm_count * kThreads));
+  const bool wide = a.cap + 1 > kMaxSmemBins || per_lane * (double)a.cap >= 2147483647.0;
   return dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, false,
                          [&](auto cfg) -> cudaError_t {
-    const bool out = o.M || o.edge || o.x || o.trunc;
     auto k = out ? native_trials_kernel<decltype(cfg), true>
                  : native_trials_kernel<decltype(cfg), false>;
     cudaError_t err = prepare(k, smem);
@@ -1225,7 +1260,7 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
     // hand-out from a warp pool kept 40 registers but cost 7%.
     return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, priv,
                   q);
-  }, inj);
+  }, inj, wide);
 }
 
 cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,

@@ -176,6 +176,15 @@ class EnsembleResult:
     config: SimulationConfig
 
 
+def available_workers() -> int:
+    """Reference ``engine.py:186-187`` (numba's thread count).  ``workers`` has
+    no effect here (the GPU runs every particle at once); this reports the
+    host's CPU count so reference code sizing its ``workers`` keeps working."""
+    import os
+
+    return int(os.cpu_count() or 1)
+
+
 def _resolve_initial(graph: MetricGraph, init: InitialDistribution):
     """Initial distribution -> placement code (reference ``engine.py:194-203``)."""
     if isinstance(init, AtVertex):

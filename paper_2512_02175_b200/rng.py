@@ -16,6 +16,23 @@ def raw64(seed: int, stream: int, index: int) -> int:
     return int(_native.lib().gsde_raw64(seed, stream, index))
 
 
+def u64_to_uniform(r: int) -> float:
+    """``(r >> 11) 2^-53`` in [0, 1) (``rng.py:69-72``)."""
+    return float(_native.lib().gsde_u64_to_uniform(int(r) & 0xFFFFFFFFFFFFFFFF))
+
+
+def norm_ppf(p: float) -> float:
+    """Standard normal quantile, AS241 with the far-tail Newton polish
+    (``rng.py:81-134``)."""
+    return float(_native.lib().gsde_norm_ppf(float(p)))
+
+
+def u64_to_normal(r: int) -> float:
+    """Normal variate of a raw word, on the centred 53-bit lattice
+    (``rng.py:137-143``)."""
+    return float(_native.lib().gsde_u64_to_normal(int(r) & 0xFFFFFFFFFFFFFFFF))
+
+
 def uniform01(seed: int, stream: int, index: int) -> float:
     return float(_native.lib().gsde_uniform01(seed, stream, index))
 

@@ -64,13 +64,9 @@ def test_norm_ppf_values():
     for row in data["normal_extremes"]:
         r = int(row["raw"])
         v = oracle.lib().orc_u64_to_normal(r)
-        if abs(row["normal"]) < 8.0:
-            assert close(v, row["normal"], 1e-14, 1e-15), row
-        else:
-            # top two lattice points (probability 2^-52): the reference's
-            # fastmath build evaluates min(p, 1-p) as (2^53 - n) 2^-53, the
-            # oracle exactly as (2^53 - n - 1/2) 2^-53; both finite, < 0.1 apart.
-            assert np.isfinite(v) and abs(v - row["normal"]) < 0.1, row
+        # incl. the top lattice points: the reference's fastmath build forms
+        # min(p, 1-p) above the median as (2^53 - n) 2^-53, and so does the oracle
+        assert close(v, row["normal"], 1e-14, 1e-15), row
 
 
 def test_first_passage_vectors():
