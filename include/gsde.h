@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define GSDE_ABI_VERSION 1
+#define GSDE_ABI_VERSION 2
 
 enum {
   GSDE_OK = 0,
@@ -52,8 +52,15 @@ enum { GSDE_STREAM_NATIVE = 0, GSDE_STREAM_REFERENCE = 1, GSDE_STREAM_INJECT = 2
  * and vertex trials. */
 enum { GSDE_PREC_F32 = 0, GSDE_PREC_F64 = 1, GSDE_PREC_NATIVE = 2 };
 
-/* Initial placement codes (kernels.py:48-50). */
-enum { GSDE_INIT_POINT = 0, GSDE_INIT_PER_EDGE_UNIFORM = 1 };
+/* Initial placement codes (kernels.py:48-50), plus per-particle state-in:
+ * GSDE_INIT_STATE takes particle i's (edge, x) from the SoA device arrays
+ * state_edge / state_x of the run arguments (read coalesced, a warp's 32 particles
+ * per refill) -- the batched form of em_step_*'s ParticleState
+ * (engine.py:60-67, :206-270) and the resume point of a checkpointed run.
+ * NATIVE and INJECT/NATIVE streams only; the caller guarantees
+ * 0 <= edge < n_edges and 0 <= x <= length (x > 0 on a star edge unless at
+ * the vertex). */
+enum { GSDE_INIT_POINT = 0, GSDE_INIT_PER_EDGE_UNIFORM = 1, GSDE_INIT_STATE = 2 };
 
 typedef struct gsde_graph_s gsde_graph; /* opaque, device-resident graph + field */
 
@@ -105,6 +112,12 @@ typedef struct {
   const uint64_t *inj_raw;    /* device [n_particles][inj_stride] */
   const double *inj_normal;   /* device [n_particles][inj_stride] */
   int64_t inj_stride;
+  /* GSDE_INIT_STATE (device, [n_particles]): edge ids, positions, and for the
+   * NATIVE stream optionally each particle's next Philox block (NULL = 0) --
+   * gsde_out.counter of the run being resumed */
+  const int32_t *state_edge;
+  const float *state_x;
+  const uint64_t *state_counter;
 } gsde_run;
 
 /* Ensemble outputs: device pointers, each optional (NULL = skip).  Per-particle
@@ -128,6 +141,11 @@ typedef struct {
   int64_t *occ;                /* [n_cells] */
   int64_t occ_every;           /* >= 1 */
   int64_t occ_start;           /* steps before the first sample (burn-in) */
+  /* [n_particles]: NATIVE -- the particle's next unused Philox block (resume
+   * with GSDE_INIT_STATE + state_counter); INJECT/NATIVE -- the number of
+   * injected draws the particle consumed (the reference's RngStream.counter
+   * advance, engine.py:228) */
+  uint64_t *counter;
 } gsde_out;
 
 /* run_ensemble's kernel call: kernels.ensemble_star / ensemble_general

@@ -262,29 +262,48 @@ typedef struct {
   int64_t M;
   int32_t trunc;
   uint64_t k;
+  /* diagnostics (not reference output): the smallest relative margin of the
+   * step's continuous decisions -- |proposal - boundary| over the magnitude
+   * of the terms that formed it (free / excursion accept tests, mirror
+   * wall), |1 - alpha| (excursion residual time), |1 - s| for a split root
+   * clamped near 1.  An FP32 evaluation can only take another branch where
+   * this is within FP32 rounding (~1e-7 of the terms). */
+  double margin;
 } orc_step_out;
+
+static inline double rel_margin(double v, double t0, double t1, double t2) {
+  double s = fabs(t0);
+  if (fabs(t1) > s) s = fabs(t1);
+  if (fabs(t2) > s) s = fabs(t2);
+  return s > 0.0 ? fabs(v) / s : INFINITY;
+}
+#define MG(m, v) do { double m_ = (v); if (m_ < (m)) (m) = m_; } while (0)
 
 /* kernels.py:146-220 (draws: N on a free step; then U,N per vertex iteration) */
 static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double dt,
                               orc_draws *d, int64_t cap, double reflect_len) {
   orc_step_out o;
   int64_t M = 0;
+  double mg = INFINITY;
   if (x > 0.0) {
     double w = orc_u64_to_normal(draw(d));
     double mu = drift_at(g, edge, x);
     double a = mu * dt;
     double b = g->sigma[edge] * sqrt(dt) * w;
     double xn = x + a + b;
+    MG(mg, rel_margin(xn, x, a, b));
     if (xn > 0.0) {
+      if (reflect_len > 0.0) MG(mg, rel_margin(xn - reflect_len, x, a, b) /* wall */);
       if (reflect_len > 0.0 && xn > reflect_len) {
         xn = 2.0 * reflect_len - xn;
         if (xn < 0.0) xn = 0.0;
       }
-      o.edge = edge; o.x = xn; o.M = 0; o.trunc = 0; o.k = d->k;
+      o.edge = edge; o.x = xn; o.M = 0; o.trunc = 0; o.k = d->k; o.margin = mg;
       return o;
     }
     double s = orc_solve_first_passage_s(a, b, x);
     if (s < 0.0) s = 1.0;
+    if (s < 1.0) MG(mg, 1.0 - s);
     dt = (1.0 - s * s) * dt;
     if (dt < 0.0) dt = 0.0;
   }
@@ -296,22 +315,26 @@ static orc_step_out step_star(const orc_graph *g, int64_t edge, double x, double
     double mu0 = drift_at(g, edge, 0.0);
     double sig0 = g->sigma[edge];
     double xn = mu0 * dt + sig0 * sqrt(dt) * fabs(w);
+    MG(mg, rel_margin(xn, mu0 * dt, sig0 * sqrt(dt) * w, 0.0));
     if (xn >= 0.0) {
+      if (reflect_len > 0.0) MG(mg, rel_margin(xn - reflect_len, mu0 * dt, sig0 * sqrt(dt) * w,
+                                                reflect_len));
       if (reflect_len > 0.0 && xn > reflect_len) {
         xn = 2.0 * reflect_len - xn;
         if (xn < 0.0) xn = 0.0;
       }
-      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = d->k;
+      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = d->k; o.margin = mg;
       return o;
     }
     double alpha = (w * w * sig0 * sig0) / (mu0 * mu0 * dt);
+    MG(mg, fabs(1.0 - alpha));
     dt = (1.0 - alpha) * dt;
     if (dt <= 0.0) {
-      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 0; o.k = d->k;
+      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 0; o.k = d->k; o.margin = mg;
       return o;
     }
     if (M >= cap) {
-      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 1; o.k = d->k;
+      o.edge = edge; o.x = 0.0; o.M = M; o.trunc = 1; o.k = d->k; o.margin = mg;
       return o;
     }
   }
@@ -322,6 +345,7 @@ static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, dou
                                  orc_draws *d, int64_t cap) {
   orc_step_out o;
   int64_t M = 0;
+  double mg = INFINITY;
   for (;;) {
     double l = g->edge_len[edge];
     if (x <= 0.0 || x >= l) {
@@ -337,8 +361,10 @@ static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, dou
     double a = mu * dt;
     double b = g->sigma[edge] * sqrt(dt) * w;
     double xn = x + a + b;
+    MG(mg, rel_margin(xn, x, a, b));
+    MG(mg, rel_margin(l - xn, l, a, b));
     if (0.0 < xn && xn < l) {
-      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = d->k;
+      o.edge = edge; o.x = xn; o.M = M; o.trunc = 0; o.k = d->k; o.margin = mg;
       return o;
     }
     ++M;
@@ -351,13 +377,14 @@ static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, dou
       x = l;
     }
     if (s < 0.0) s = 1.0;
+    if (s < 1.0) MG(mg, 1.0 - s);
     dt = (1.0 - s * s) * dt;
     if (dt <= 0.0) {
-      o.edge = edge; o.x = x; o.M = M; o.trunc = 0; o.k = d->k;
+      o.edge = edge; o.x = x; o.M = M; o.trunc = 0; o.k = d->k; o.margin = mg;
       return o;
     }
     if (M >= cap) {
-      o.edge = edge; o.x = x; o.M = M; o.trunc = 1; o.k = d->k;
+      o.edge = edge; o.x = x; o.M = M; o.trunc = 1; o.k = d->k; o.margin = mg;
       return o;
     }
   }
@@ -366,13 +393,37 @@ static orc_step_out step_general(const orc_graph *g, int64_t edge, double x, dou
 /* Single step, the per-step golden oracle (engine.py:206-270). */
 void orc_step(const orc_graph *g, int32_t star, int64_t edge, double x, double dt,
               uint64_t seed, uint64_t pid, uint64_t k, int64_t cap, double reflect_len,
-              int64_t *o_edge, double *o_x, int64_t *o_M, int32_t *o_trunc, uint64_t *o_k) {
+              int64_t *o_edge, double *o_x, int64_t *o_M, int32_t *o_trunc, uint64_t *o_k,
+              double *o_margin) {
   orc_draws d;
   draws_init(&d, seed, pid, k);
   orc_step_out o = star ? step_star(g, edge, x, dt, &d, cap, reflect_len)
                         : step_general(g, edge, x, dt, &d, cap);
   *o_edge = o.edge; *o_x = o.x; *o_M = o.M; *o_trunc = o.trunc; *o_k = o.k;
+  if (o_margin) *o_margin = o.margin;
 }
+
+/* Batched single steps from per-row states and streams (the golden em_step
+ * rows) with each step's decision margin. */
+void orc_step_rows(const orc_graph *g, int32_t star, int64_t n, const int64_t *edge,
+                   const double *x, const double *dt, const uint64_t *seed, const uint64_t *pid,
+                   const uint64_t *k, const int64_t *cap, const double *reflect_len,
+                   int64_t *o_edge, double *o_x, int64_t *o_M, int32_t *o_trunc, uint64_t *o_k,
+                   double *o_margin) {
+  for (int64_t i = 0; i < n; ++i)
+    orc_step(g, star, edge[i], x[i], dt[i], seed[i], pid[i], k[i], cap[i], reflect_len[i],
+             o_edge + i, o_x + i, o_M + i, o_trunc + i, o_k + i, o_margin + i);
+}
+
+/* Whole trajectories recorded per step (run_ensemble's particles,
+ * kernels.py:310-444): after step s of particle i, [i * n_steps + s] holds
+ * the edge, position, M, truncation flag, next draw index and the step's
+ * decision margin. */
+void orc_trace(const orc_graph *g, int32_t star, uint64_t seed, int64_t n_particles,
+               int64_t pid_offset, int64_t n_steps, double dt, int32_t init_kind,
+               int64_t init_edge, double init_x, double init_xmax, int64_t cap,
+               double reflect_len, int64_t *t_edge, double *t_x, int64_t *t_M, int32_t *t_trunc,
+               uint64_t *t_k, double *t_margin, int32_t n_threads);
 
 /* kernels.py:291-307 */
 static void place(const orc_graph *g, uint64_t seed, uint64_t pid, int32_t init_kind,
@@ -432,6 +483,34 @@ void orc_ensemble(const orc_graph *g, int32_t star, uint64_t seed, int64_t n_par
       if (out_cross) out_cross[i] = cross;
       if (out_events) out_events[i] = events;
       if (out_trunc) out_trunc[i] = truncs;
+    }
+  }
+}
+
+void orc_trace(const orc_graph *g, int32_t star, uint64_t seed, int64_t n_particles,
+               int64_t pid_offset, int64_t n_steps, double dt, int32_t init_kind,
+               int64_t init_edge, double init_x, double init_xmax, int64_t cap,
+               double reflect_len, int64_t *t_edge, double *t_x, int64_t *t_M, int32_t *t_trunc,
+               uint64_t *t_k, double *t_margin, int32_t n_threads) {
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(dynamic, 64)
+#endif
+  for (int64_t i = 0; i < n_particles; ++i) {
+    uint64_t pid = (uint64_t)(i + pid_offset);
+    int64_t edge;
+    double x;
+    uint64_t k;
+    place(g, seed, pid, init_kind, init_edge, init_x, init_xmax, &edge, &x, &k);
+    orc_draws d;
+    draws_init(&d, seed, pid, k);
+    for (int64_t s = 0; s < n_steps; ++s) {
+      orc_step_out o = star ? step_star(g, edge, x, dt, &d, cap, reflect_len)
+                            : step_general(g, edge, x, dt, &d, cap);
+      edge = o.edge; x = o.x;
+      const int64_t j = i * n_steps + s;
+      t_edge[j] = edge; t_x[j] = x; t_M[j] = o.M; t_trunc[j] = o.trunc; t_k[j] = o.k;
+      t_margin[j] = o.margin;
     }
   }
 }

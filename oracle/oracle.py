@@ -57,7 +57,10 @@ def lib():
         L.orc_solve_first_passage_s.argtypes = [f64, f64, f64]
         L.orc_philox4x32_10.argtypes = [P, P, P]
         L.orc_step.argtypes = [C.POINTER(_Graph), i32, i64, f64, f64, u64, u64, u64, i64, f64,
-                               P, P, P, P, P]
+                               P, P, P, P, P, P]
+        L.orc_step_rows.argtypes = [C.POINTER(_Graph), i32, i64] + [P] * 15
+        L.orc_trace.argtypes = [C.POINTER(_Graph), i32, u64, i64, i64, i64, f64, i32, i64, f64,
+                                f64, i64, f64, P, P, P, P, P, P, i32]
         L.orc_ensemble.argtypes = [C.POINTER(_Graph), i32, u64, i64, i64, i64, f64, i32, i64,
                                    f64, f64, i64, f64, P, P, P, P, P, P, i32]
         L.orc_vertex_trials.argtypes = [C.POINTER(_Graph), i32, u64, i64, i64, f64, i64, f64,
@@ -142,8 +145,37 @@ def step(og: OracleGraph, edge, x, dt, seed, pid, k, cap=100, reflect_len=0.0):
     e = np.zeros(1, np.int64); xo = np.zeros(1); M = np.zeros(1, np.int64)
     tr = np.zeros(1, np.int32); ko = np.zeros(1, np.uint64)
     lib().orc_step(C.byref(og.c), int(og.is_star), edge, x, dt, seed, pid, k, cap, reflect_len,
-                   _ptr(e), _ptr(xo), _ptr(M), _ptr(tr), _ptr(ko))
+                   _ptr(e), _ptr(xo), _ptr(M), _ptr(tr), _ptr(ko), None)
     return int(e[0]), float(xo[0]), int(M[0]), bool(tr[0]), int(ko[0])
+
+
+def step_rows(og: OracleGraph, edge, x, dt, seed, pid, k, cap, reflect_len):
+    """Per-row single steps (arrays of equal length n) -> dict of outputs incl.
+    each step's decision ``margin`` (smallest relative distance of a
+    continuous decision from its threshold; see orc_step_out)."""
+    n = len(edge)
+    a = lambda v, t: np.ascontiguousarray(np.broadcast_to(np.asarray(v, t), (n,)))
+    ins = [a(edge, np.int64), a(x, np.float64), a(dt, np.float64), a(seed, np.uint64),
+           a(pid, np.uint64), a(k, np.uint64), a(cap, np.int64), a(reflect_len, np.float64)]
+    out = dict(edge=np.zeros(n, np.int64), x=np.zeros(n), M=np.zeros(n, np.int64),
+               trunc=np.zeros(n, np.int32), k=np.zeros(n, np.uint64), margin=np.zeros(n))
+    lib().orc_step_rows(C.byref(og.c), int(og.is_star), n, *[_ptr(v) for v in ins],
+                        *[_ptr(out[q]) for q in ("edge", "x", "M", "trunc", "k", "margin")])
+    return out
+
+
+def trace(og: OracleGraph, seed, n, n_steps, dt, init=(0, 0, 0.0, 0.0), cap=100,
+          reflect_len=0.0, pid_offset=0, threads=0):
+    """Whole reference trajectories recorded after every step: arrays
+    ``[n, n_steps]`` of edge, x, M, trunc, next draw index k and margin."""
+    init_kind, init_edge, init_x, init_xmax = init
+    out = dict(edge=np.zeros((n, n_steps), np.int64), x=np.zeros((n, n_steps)),
+               M=np.zeros((n, n_steps), np.int64), trunc=np.zeros((n, n_steps), np.int32),
+               k=np.zeros((n, n_steps), np.uint64), margin=np.zeros((n, n_steps)))
+    lib().orc_trace(C.byref(og.c), int(og.is_star), seed, n, pid_offset, n_steps, dt, init_kind,
+                    init_edge, init_x, init_xmax, cap, reflect_len,
+                    *[_ptr(out[q]) for q in ("edge", "x", "M", "trunc", "k", "margin")], threads)
+    return out
 
 
 CHUNK = 4096

@@ -27,6 +27,7 @@ GSDE_PREC_F64 = 1
 GSDE_PREC_NATIVE = 2  # INJECT into the production FP32 kernel (ensembles)
 GSDE_INIT_POINT = 0
 GSDE_INIT_PER_EDGE_UNIFORM = 1
+GSDE_INIT_STATE = 2
 
 _P = C.c_void_p
 _i64, _u64, _f64, _i32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32
@@ -58,6 +59,7 @@ class Run(C.Structure):
         ("dt", _f64), ("init_kind", _i32), ("init_edge", _i64), ("init_x", _f64),
         ("init_xmax", _f64), ("cap", _i32), ("reflect_len", _f64), ("stream", _i32),
         ("precision", _i32), ("inj_raw", _P), ("inj_normal", _P), ("inj_stride", _i64),
+        ("state_edge", _P), ("state_x", _P), ("state_counter", _P),
     ]
 
 
@@ -66,7 +68,7 @@ class Out(C.Structure):
         ("edge", _P), ("crossings", _P), ("events", _P), ("truncs", _P), ("x", _P),
         ("m_hist", _P), ("totals", _P), ("edge_counts", _P), ("hist", _P),
         ("hist_offsets", _P), ("hist_counts", _P), ("hist_dx", _P), ("hist_n_cells", _i64),
-        ("occ", _P), ("occ_every", _i64), ("occ_start", _i64),
+        ("occ", _P), ("occ_every", _i64), ("occ_start", _i64), ("counter", _P),
     ]
 
 
@@ -149,7 +151,7 @@ def lib():
                 L.gsde_parsed_free.restype = None
                 L.gsde_launch_count.restype = _i64
                 L.gsde_last_error.restype = C.c_char_p
-                assert L.gsde_abi_version() == 1, "libgsde ABI mismatch"
+                assert L.gsde_abi_version() == 2, "libgsde ABI mismatch"
                 _lib = L
     return _lib
 

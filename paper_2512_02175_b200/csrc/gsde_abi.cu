@@ -405,8 +405,21 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
   if (a->cap < 1) return set_error(GSDE_EINVAL, "ensemble: cap must be >= 1");
   if (a->reflect_len < 0.0 || (a->reflect_len > 0.0 && !g->is_star))
     return set_error(GSDE_EINVAL, "ensemble: reflect_len applies to star graphs only");
-  if (a->init_kind != GSDE_INIT_POINT && a->init_kind != GSDE_INIT_PER_EDGE_UNIFORM)
+  if (a->init_kind != GSDE_INIT_POINT && a->init_kind != GSDE_INIT_PER_EDGE_UNIFORM &&
+      a->init_kind != GSDE_INIT_STATE)
     return set_error(GSDE_EINVAL, "ensemble: bad init_kind %d", a->init_kind);
+  if (a->init_kind == GSDE_INIT_STATE) {
+    if (!a->state_edge || !a->state_x)
+      return set_error(GSDE_EINVAL, "ensemble: GSDE_INIT_STATE needs state_edge and state_x");
+    if (!(a->stream == GSDE_STREAM_NATIVE ||
+          (a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE)))
+      return set_error(GSDE_EINVAL, "ensemble: GSDE_INIT_STATE runs the NATIVE or "
+                                    "INJECT/NATIVE streams (REFERENCE states: gsde_step_batch)");
+  }
+  if (o->counter && !(a->stream == GSDE_STREAM_NATIVE ||
+                      (a->stream == GSDE_STREAM_INJECT && a->precision == GSDE_PREC_NATIVE)))
+    return set_error(GSDE_EINVAL, "ensemble: the counter output is a NATIVE / INJECT-NATIVE "
+                                  "output");
   if (a->init_kind == GSDE_INIT_POINT && (a->init_edge < 0 || a->init_edge >= g->E))
     return set_error(GSDE_EINVAL, "ensemble: init_edge out of range");
   if ((o->hist || o->occ) && (!o->hist_offsets || !o->hist_counts || !o->hist_dx ||

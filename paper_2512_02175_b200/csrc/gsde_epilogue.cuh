@@ -25,7 +25,7 @@ __device__ __forceinline__ int64_t hist_cell(const int64_t *offsets, const int64
 }
 
 // Per-particle result arrays of one ensemble particle (kernels.py:370-374).
-__device__ __forceinline__ void epilogue_particle(const gsde_out &o, int64_t i, int e, double x,
+__device__ __forceinline__ void epilogue_particle(const KOut &o, int64_t i, int e, double x,
                                                   int64_t cross, int64_t events,
                                                   int64_t truncs) {
   if (o.edge) o.edge[i] = e;
@@ -37,12 +37,12 @@ __device__ __forceinline__ void epilogue_particle(const gsde_out &o, int64_t i, 
 
 // Fused estimators of one final state: final-edge occupancy and the snapshot
 // histogram (analysis.py:61-79).
-__device__ __forceinline__ void epilogue_bins(const gsde_out &o, int e, double x) {
+__device__ __forceinline__ void epilogue_bins(const KOut &o, int e, double x) {
   if (o.edge_counts) add_i64(&o.edge_counts[e], 1);
   if (o.hist) add_i64(&o.hist[hist_cell(o.hist_offsets, o.hist_counts, o.hist_dx, e, x)], 1);
 }
 
-__device__ __forceinline__ void ensemble_epilogue(const gsde_out &o, int64_t i, int e, double x,
+__device__ __forceinline__ void ensemble_epilogue(const KOut &o, int64_t i, int e, double x,
                                                   int64_t cross, int64_t events,
                                                   int64_t truncs) {
   epilogue_particle(o, i, e, x, cross, events, truncs);

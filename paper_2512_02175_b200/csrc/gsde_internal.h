@@ -35,6 +35,30 @@ struct gsde_graph_s {
 
 namespace gsde {
 
+// Kernel-side view of gsde_out: the estimator / output pointers the ensemble
+// kernels take by value.  Its layout is deliberately frozen -- the kernel
+// parameter layout feeds the register allocator, and growing this struct
+// moved the headline kernel from 64 to 67 registers (one CTA per SM fewer).
+// Later outputs (the per-particle counter) travel in the kernels' last
+// parameter instead.
+struct KOut {
+  int64_t *edge, *crossings, *events, *truncs;
+  double *x;
+  int64_t *m_hist, *totals, *edge_counts, *hist;
+  const int64_t *hist_offsets, *hist_counts;
+  const double *hist_dx;
+  int64_t hist_n_cells;
+  int64_t *occ;
+  int64_t occ_every, occ_start;
+};
+
+inline KOut kernel_out(const gsde_out &o) {
+  return KOut{o.edge,        o.crossings,   o.events,   o.truncs,       o.x,
+              o.m_hist,      o.totals,      o.edge_counts, o.hist,      o.hist_offsets,
+              o.hist_counts, o.hist_dx,     o.hist_n_cells, o.occ,      o.occ_every,
+              o.occ_start};
+}
+
 // Per-call device properties (cached per device).
 struct DevInfo {
   int sm_count = 0;

@@ -81,6 +81,14 @@ struct InjParams {
   const uint64_t *thresh;
   const int32_t *vedges;
   const uint8_t *vorient;
+  // FULL / INJ kernels (the last kernel parameter, so it may grow without
+  // moving the others -- see KOut): GSDE_INIT_STATE's per-particle SoA state,
+  // the NATIVE stream's next Philox block per particle, and the per-particle
+  // counter output
+  const int32_t *st_e;
+  const float *st_x;
+  const uint64_t *st_k;
+  uint64_t *counter;
 };
 
 __device__ __forceinline__ float fast_sqrt(float v) {
@@ -197,7 +205,7 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 
 // Compile-time kernel variant.
 template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false,
-          bool INJ_ = false, bool WIDE_ = false>
+          bool INJ_ = false, bool FULL_ = false>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
@@ -208,12 +216,15 @@ struct Cfg {
   // parity mode: the production kernel fed the reference's injected draws
   // (one per use, in the reference's order) and its inverse-CDF exit slots
   static constexpr bool INJ = INJ_;
-  // long / high-cap runs (chosen by the host only when a 32-bit per-lane
-  // count, the shared M-histogram or the 32-bit Philox block index could
-  // overflow): int64 per-particle counters, M bins beyond kMaxSmemBins in
-  // global memory, 64-bit block index.  Common runs keep the 32-bit kernel.
-  static constexpr bool WIDE = WIDE_;
-  using Cnt = std::conditional_t<WIDE_, long long, int>;
+  // The full-featured kernel, chosen by the host only when a run needs it:
+  // int64 per-particle counts, M bins beyond kMaxSmemBins in global memory and
+  // a 64-bit Philox block index (runs where a 32-bit one could overflow),
+  // per-particle state-in (GSDE_INIT_STATE) and the per-particle counter
+  // output (resume).  The common configuration keeps the lean kernel, whose
+  // register allocation the extra code would otherwise perturb.
+  static constexpr bool FULL = FULL_;
+  static constexpr bool STATE = FULL_ || INJ_;  // state-in / counter out compiled in
+  using Cnt = std::conditional_t<FULL_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
 };
 
@@ -250,15 +261,15 @@ constexpr int kOccTabEdges = 1024;  // per-edge occupation records staged in sha
 struct Shared {
   int *priv;                 // [kPriv][kThreads]
   int *mh;                   // [min(cap+1, kMaxSmemBins)]
-  int nbs;                   // M bins in shared memory (WIDE kernels: the rest in mh_g)
-  int64_t *mh_g;             // the call's M histogram (global; WIDE kernels)
+  int nbs;                   // M bins in shared memory (FULL kernels: the rest in mh_g)
+  int64_t *mh_g;             // the call's M histogram (global; FULL kernels)
   unsigned long long *tot;   // [4]
   int *exit_priv;            // trials: [E][kThreads] or null
   unsigned *occ;             // [n_cells] or null
 };
 
 // M-histogram bins kept in shared memory: caps up to 8191 (32 KB); a larger
-// cap (the reference accepts any) selects a WIDE kernel, which counts the
+// cap (the reference accepts any) selects a FULL kernel, which counts the
 // bins beyond in global memory
 constexpr int kMaxSmemBins = 8192;
 __host__ __device__ __forceinline__ int smem_bins(int nb) {
@@ -269,17 +280,17 @@ __device__ __forceinline__ size_t shared_head_bytes(int nbs) {
   return align16((size_t)(kPriv * kThreads + nbs) * sizeof(int)) + 4 * sizeof(unsigned long long);
 }
 
-// (WIDE: the shared M bins are capped at kMaxSmemBins; otherwise the host
+// (FULL: the shared M bins are capped at kMaxSmemBins; otherwise the host
 // guarantees cap + 1 <= kMaxSmemBins)
-template <bool STAR, bool SMEM, bool WIDE = false>
+template <bool STAR, bool SMEM, bool FULL = false>
 __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64_t *m_hist,
                                              Shared &S, Tables<SMEM> &T, bool exit_priv,
                                              int occ_cells) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int nbs = WIDE ? smem_bins(nb) : nb;
+  const int nbs = FULL ? smem_bins(nb) : nb;
   S.priv = reinterpret_cast<int *>(smem);
   S.mh = S.priv + kPriv * kThreads;
-  if (WIDE) {
+  if (FULL) {
     S.nbs = nbs;
     S.mh_g = m_hist;
   }
@@ -322,21 +333,21 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64
   __syncthreads();
 }
 
-template <bool WIDE>
+template <bool FULL>
 __device__ __forceinline__ void mh_add(const Shared &S, int bin) {
   if (bin < kPriv)
     S.priv[bin * kThreads + threadIdx.x] += 1;
-  else if (!WIDE || bin < S.nbs)
+  else if (!FULL || bin < S.nbs)
     atomicAdd(&S.mh[bin], 1);
   else if (S.mh_g)
     add_i64(&S.mh_g[bin], 1);
 }
 
-template <bool WIDE = false>
+template <bool FULL = false>
 __device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int occ_cells,
                              int64_t *occ_out) {
   __syncthreads();
-  const int nbs = WIDE ? smem_bins(nb) : nb;
+  const int nbs = FULL ? smem_bins(nb) : nb;
   for (int b = threadIdx.x; b < nbs; b += blockDim.x) {
     int64_t v = S.mh[b];
     if (b < kPriv)
@@ -444,7 +455,7 @@ struct Lane {
       cross += M;
       events += 1;
       truncs += trunc ? 1 : 0;
-      mh_add<C::WIDE>(S, M > cap ? cap : M);
+      mh_add<C::FULL>(S, M > cap ? cap : M);
     }
     M = 0;
     trunc = false;
@@ -646,6 +657,9 @@ __device__ __forceinline__ void place_values(const NativeGraph &G, const Tables<
   if (p.init_kind == GSDE_INIT_POINT) {
     e = p.init_edge;
     x = fminf(p.init_x, T.E(e).x);  // the FP32 edge, like every native position
+  } else if (C::STATE && p.init_kind == GSDE_INIT_STATE) {
+    e = __ldg(q.st_e + i);  // coalesced: a warp refills 32 consecutive ids
+    x = __ldg(q.st_x + i);
   } else if constexpr (C::INJ) {
     const uint64_t *r = q.raw + i * q.stride;
     place_from_raw<C::SMEM>(G, T, p, __ldg(r), __ldg(r + 1), e, x);
@@ -730,7 +744,7 @@ struct IterWords {
 // warp) measured +4% over 4 blocks / 64 registers; general graphs keep 4.
 template <class C, int Q, int SLOTS>
 __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlocks)
-    native_ensemble_kernel(NativeGraph G, NatParams p, gsde_out o, int occ_smem_cells,
+    native_ensemble_kernel(NativeGraph G, NatParams p, KOut o, int occ_smem_cells,
                            unsigned long long *work, unsigned queue_off,
                            unsigned occ_tab_off, InjParams q) {
   using IW = IterWords<Q, SLOTS>;
@@ -738,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM, C::WIDE>(G, nb, o.m_hist, S, T, false,
+  shared_setup<C::STAR, C::SMEM, C::FULL>(G, nb, o.m_hist, S, T, false,
                                           C::OCC ? occ_smem_cells : 0);
   Occ O{o.hist_offsets, o.hist_counts, o.hist_dx, o.occ, S.occ, (int32_t)o.occ_every,
         (int32_t)o.occ_start, nullptr};
@@ -765,7 +779,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   L.steps_left = 0;  // no particle in flight: every trip is a no-op
   L.occ_left = 1 << 30;
   // Per-particle Philox block index: 32 bits in the counter's first word.
-  // WIDE kernels (runs that could pass 2^32 blocks per particle) carry the
+  // FULL kernels (runs that could pass 2^32 blocks per particle) carry the
   // wrap into bits 48.. of the stream-id word -- particle ids stay below 2^48
   // (checked by the host) -- so streams never repeat.
   uint32_t blk = 0;
@@ -783,6 +797,8 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     t_truncs += L.truncs;
     if (C::INJ) t_over += L.over ? 1 : 0;
     epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
+    if (C::STATE && q.counter)  // next block (NATIVE: carry in id's bits 48..) / draws used (INJ)
+      q.counter[i] = C::INJ ? (uint64_t)L.k : ((id >> 48) << 32) | blk;
     queued = true;
     active = false;
     need = true;
@@ -878,11 +894,17 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
             L.vor = q.vorient;
             L.ir = q.raw + i * q.stride;
             L.inn = q.normal + i * q.stride;
-            L.k = p.init_kind == GSDE_INIT_POINT ? 0 : 2;  // placement used draws 0, 1
+            // PerEdgeUniform placement used the row's draws 0 and 1
+            L.k = p.init_kind == GSDE_INIT_PER_EDGE_UNIFORM ? 2 : 0;
             L.kmax = (int)q.stride;
             L.over = false;
           }
           blk = 0;
+          if (C::STATE && p.init_kind == GSDE_INIT_STATE && q.st_k) {  // resume: next block
+            const uint64_t k0 = __ldg(q.st_k + i);
+            blk = (uint32_t)k0;
+            id += (k0 >> 32) << 48;
+          }
           waiting = false;
           active = true;
         }
@@ -922,7 +944,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
         trip<C, false>(L, G, T, S, O, p, z1, 0u);
     }
     blk += NB;
-    if (C::WIDE && blk == 0u) id += 1ull << 48;
+    if (C::FULL && blk == 0u) id += 1ull << 48;
     if (active && L.steps_left == 0) finish();
   }
   if (bins && f_n > 0) flush_bins(f_n);
@@ -932,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     warp_add_i64(&o.totals[2], t_truncs);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush<C::WIDE>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
+  shared_flush<C::FULL>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
 }
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
@@ -944,7 +966,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM, C::WIDE>(G, nb, o.m_hist, S, T, exit_priv != 0, 0);
+  shared_setup<C::STAR, C::SMEM, C::FULL>(G, nb, o.m_hist, S, T, exit_priv != 0, 0);
   const Occ O{};
   const float inf = __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -953,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   Lane<C> L;
   uint32_t pair = 0;
   uint64_t id = 0;
-  // per-lane sums: trials per lane x cap < 2^31 unless the host chose WIDE
+  // per-lane sums: trials per lane x cap < 2^31 unless the host chose FULL
   typename C::Cnt t_M = 0;
   int32_t t_ev = 0, t_tr = 0, t_over = 0;
   auto start = [&]() {
@@ -989,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
       S.exit_priv[L.e * kThreads + threadIdx.x] += 1;
     else if (o.exit_counts)
       add_i64(&o.exit_counts[L.e], 1);
-    mh_add<C::WIDE>(S, L.M > p.cap ? p.cap : L.M);
+    mh_add<C::FULL>(S, L.M > p.cap ? p.cap : L.M);
     t_M += L.M;
     t_ev += L.M > 0 ? 1 : 0;
     t_tr += L.trunc ? 1 : 0;
@@ -1023,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     warp_add_i64(&o.totals[2], t_tr);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush<C::WIDE>(S, nb, o.m_hist, 0, nullptr);
+  shared_flush<C::FULL>(S, nb, o.m_hist, 0, nullptr);
   if (S.exit_priv && o.exit_counts) {
     for (int e = threadIdx.x; e < G.n_edges; e += blockDim.x) {
       int64_t v = 0;
@@ -1114,7 +1136,7 @@ cudaError_t prepare(K kernel, size_t smem) {
 // Runtime flags -> compile-time kernel variant (Cfg).
 template <bool OCC, class F>
 cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
-                     bool inj = false, bool wide = false) {
+                     bool inj = false, bool full = false) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
@@ -1123,14 +1145,14 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
       constexpr bool RF = decltype(rf)::value;
       if (inj) {  // parity mode: no occupation sampling, 32-bit counts
         if constexpr (!OCC) {
-          if (wide) return cudaErrorInvalidValue;
+          // (INJ kernels carry state-in and the counter; 32-bit counts)
           if (tab) return f(Cfg<ST, SM, true, RF, false, false, true>{});
           return zd ? f(Cfg<ST, SM, false, RF, false, true, true>{})
                     : f(Cfg<ST, SM, false, RF, false, false, true>{});
         }
         return cudaErrorInvalidValue;
       }
-      if (wide) {
+      if (full) {
         if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, true>{});
         return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, true>{})
                   : f(Cfg<ST, SM, false, RF, OCC, false, false, true>{});
@@ -1146,12 +1168,14 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
   return smem ? with(N{}, T{}) : with(N{}, N{});
 }
 
-// Ensembles whose 32-bit per-lane counts, shared M histogram or Philox block
-// index could overflow take the WIDE kernel: per particle at most n_steps x
-// cap crossings, and at most (cap + 2) iterations (4 blocks each) per step.
-bool ensemble_needs_wide(const gsde_run &a) {
+// Ensembles take the FULL kernel for state-in / counter output, or when a
+// 32-bit per-lane count, the shared M histogram or the Philox block index
+// could overflow: per particle at most n_steps x cap crossings, and at most
+// (cap + 2) iterations (4 blocks each) per step.
+bool ensemble_needs_full(const gsde_run &a, const gsde_out &o) {
   const double steps = (double)a.n_steps, cap = (double)a.cap;
-  return a.cap + 1 > kMaxSmemBins || steps * cap >= 2147483647.0 ||
+  return a.init_kind == GSDE_INIT_STATE || o.counter != nullptr ||
+         a.cap + 1 > kMaxSmemBins || steps * cap >= 2147483647.0 ||
          4.0 * steps * (cap + 2.0) >= 4294967296.0;
 }
 
@@ -1167,8 +1191,10 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   p.init_x = (float)a.init_x;
   p.init_xmax = a.init_xmax;
   const bool inj = a.stream == GSDE_STREAM_INJECT;  // (precision GSDE_PREC_NATIVE)
-  const InjParams q{a.inj_raw,        a.inj_normal,       a.inj_stride,
-                    g->ref32.v_thresh, g->ref32.v_edges, g->ref32.v_orient};
+  const InjParams q{a.inj_raw,         a.inj_normal,       a.inj_stride,
+                    g->ref32.v_thresh, g->ref32.v_edges,   g->ref32.v_orient,
+                    a.state_edge,      a.state_x,          a.state_counter,
+                    o.counter};
   const bool stage = g->nat_graph_smem > 0;
   const bool occ = o.occ != nullptr;
   const int d = g->device;
@@ -1216,16 +1242,16 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     // (placement-only runs: 0x7f7f... -- past every particle id, nothing handed out)
     err = cudaMemsetAsync(work, a.n_steps == 0 ? 0x7f : 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
-    err = launch(k, smem, grid, s, g->nat, p, o, occ_cells, work, (unsigned)qoff,
+    err = launch(k, smem, grid, s, g->nat, p, kernel_out(o), occ_cells, work, (unsigned)qoff,
                  (unsigned)(qoff + queues), q);
     if (err != cudaSuccess) return err;
     return cudaEventRecord(done, s);
   };
-  const bool wide = ensemble_needs_wide(a);
+  const bool full = ensemble_needs_full(a, o);
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
-                              inj, wide)
+                              inj, full)
              : dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                               run, inj, wide);
+                               run, inj, full);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
@@ -1242,10 +1268,10 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   const InjParams q{a.inj_raw,        a.inj_normal,       a.inj_stride,
                     g->ref32.v_thresh, g->ref32.v_edges, g->ref32.v_orient};
   const bool out = o.M || o.edge || o.x || o.trunc;
-  // WIDE when a lane's sum of M (<= its trials x cap; conservatively one
+  // FULL when a lane's sum of M (<= its trials x cap; conservatively one
   // block per SM) could pass 2^31 or the M histogram outgrows shared memory
   const double per_lane = std::ceil((double)n / ((double)dev_info(d).sm_count * kThreads));
-  const bool wide = a.cap + 1 > kMaxSmemBins || per_lane * (double)a.cap >= 2147483647.0;
+  const bool full = a.cap + 1 > kMaxSmemBins || per_lane * (double)a.cap >= 2147483647.0;
   return dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, false,
                          [&](auto cfg) -> cudaError_t {
     auto k = out ? native_trials_kernel<decltype(cfg), true>
@@ -1260,7 +1286,7 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
     // hand-out from a warp pool kept 40 registers but cost 7%.
     return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, priv,
                   q);
-  }, inj, wide);
+  }, inj, full);
 }
 
 cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,

@@ -233,7 +233,7 @@ __device__ __forceinline__ void place(const RefGraph<R> &g, const gsde_run &a, D
 
 template <class R, class D, bool STAR>
 __global__ void __launch_bounds__(256) ref_ensemble_kernel(RefGraph<R> g, gsde_run a,
-                                                           gsde_out o, int mh_smem) {
+                                                           KOut o, int mh_smem) {
   extern __shared__ int s_mh[];
   const int nb = a.cap + 1;
   if (mh_smem)
@@ -369,9 +369,9 @@ cudaError_t ensemble_impl(const RefGraph<R> &g, bool star, const gsde_run &a, co
   const int use_smem = mh <= 32 * 1024 ? 1 : 0;
   const int grid = grid_for(a.n_particles, device);
   if (star)
-    ref_ensemble_kernel<R, D, true><<<grid, 256, use_smem ? mh : 0, s>>>(g, a, o, use_smem);
+    ref_ensemble_kernel<R, D, true><<<grid, 256, use_smem ? mh : 0, s>>>(g, a, kernel_out(o), use_smem);
   else
-    ref_ensemble_kernel<R, D, false><<<grid, 256, use_smem ? mh : 0, s>>>(g, a, o, use_smem);
+    ref_ensemble_kernel<R, D, false><<<grid, 256, use_smem ? mh : 0, s>>>(g, a, kernel_out(o), use_smem);
   count_launch();
   return cudaGetLastError();
 }

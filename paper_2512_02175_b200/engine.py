@@ -211,7 +211,8 @@ def _check_ensemble_shape(graph: MetricGraph, config: SimulationConfig) -> None:
 
 
 def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, outputs=("all",),
-                    grid=None, inject=None, precision="f32", stream=None, occupation=None):
+                    grid=None, inject=None, precision="f32", stream=None, occupation=None,
+                    state=None):
     """Run an ensemble and return DEVICE tensors (no host copies).
 
     ``outputs``: any of ``"edge", "x", "crossings", "events", "truncs"`` or
@@ -226,6 +227,17 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
     start)`` (needs ``grid``) adds the time-integrated occupation histogram
     ``res["occ"]``: every particle's (edge, x) binned after every
     ``every``-th completed macro step beyond step ``start``.
+
+    ``state=(edge, x[, counter])`` (device tensors ``[n]``) starts particle
+    ``i`` from ``(edge[i], x[i])`` instead of ``config.initial`` -- the batched
+    ``ParticleState`` of ``em_step_*`` (``engine.py:60-67``): the production
+    kernel reads it as SoA (int32 edges, float32 positions) with coalesced
+    loads.  With the native stream ``counter`` (uint64 as int64) is each
+    particle's next Philox block -- ``res["counter"]`` of the run being
+    resumed (``outputs`` incl. ``"counter"``); with ``inject`` and
+    ``precision="native"`` the injected rows start at the state's draw and
+    ``res["counter"]`` counts the draws each particle consumed.  Native /
+    injected-native streams only.
     """
     torch, dev = _native.torch_cuda(config.device)
     n = config.n_particles if n_particles is None else int(n_particles)
@@ -243,6 +255,7 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
         return None
 
     e_t, x_t = maybe("edge", torch.int64), maybe("x", torch.float64)
+    k_t = res["counter"] = torch.empty(n, dtype=torch.int64, **kw) if "counter" in want else None
     c_t, ev_t, tr_t = (maybe("crossings", torch.int64), maybe("events", torch.int64),
                        maybe("truncs", torch.int64))
     res["m_hist"] = torch.zeros(cap + 1, dtype=torch.int64, **kw)
@@ -253,7 +266,7 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
     o = _native.Out()
     for k, t in (("edge", e_t), ("x", x_t), ("crossings", c_t), ("events", ev_t),
                  ("truncs", tr_t), ("m_hist", res["m_hist"]), ("totals", res["totals"]),
-                 ("edge_counts", ec_t)):
+                 ("edge_counts", ec_t), ("counter", k_t)):
         setattr(o, k, _native.ptr(t))
     if occupation is not None and grid is None:
         raise ConfigInvalid("the occupation histogram needs a grid")
@@ -287,6 +300,18 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
         r.precision = {"f64": _native.GSDE_PREC_F64, "f32": _native.GSDE_PREC_F32,
                        "native": _native.GSDE_PREC_NATIVE}[precision]
         r.inj_raw, r.inj_normal, r.inj_stride = raw.data_ptr(), nrm.data_ptr(), raw.shape[1]
+    if state is not None:
+        se = state[0].to(device=f"cuda:{dev}", dtype=torch.int32).contiguous()
+        sx = state[1].to(device=f"cuda:{dev}", dtype=torch.float32).contiguous()
+        if se.shape[0] != n or sx.shape[0] != n:
+            raise ConfigInvalid(f"state arrays must have n_particles = {n} entries")
+        res["_state"] = (se, sx)  # alive until the launch is queued
+        r.init_kind = _native.GSDE_INIT_STATE
+        r.state_edge, r.state_x = se.data_ptr(), sx.data_ptr()
+        if len(state) > 2 and state[2] is not None:
+            sk = state[2].to(device=f"cuda:{dev}", dtype=torch.int64).contiguous()
+            res["_state"] += (sk,)
+            r.state_counter = sk.data_ptr()
     s = stream if stream is not None else _native.cur_stream(dev)
     _native.check(_native.lib().gsde_ensemble(dg.handle, r, o, s))
     return res

@@ -1,0 +1,204 @@
+"""North-star FP32 parity contract on the PRODUCTION kernel.
+
+The native FP32 ensemble kernel (Q-trip iterations, vertex slots, deferred
+split roots, alias-free inverse-CDF exits in its INJECT/NATIVE build) reads
+per-particle state through its SoA state-in path (``GSDE_INIT_STATE``: int32
+edges + float32 positions, coalesced per warp refill) and takes the
+reference's own draws in the reference's order.  Against the reference:
+
+1. every golden ``em_step_*`` row (4800 rows over 12 graphs, caps 1/3/100,
+   mirror walls; produced by the reference itself) replayed as ONE step of
+   the production kernel from the row's state: edge id, M, truncation and the
+   number of draws consumed (the reference's RngStream counter advance) equal;
+   ``|dx| <= 1e-5 max(|x|, |x'|, sigma sqrt(dt))``.  A row that disagrees must
+   be a near-tie: the oracle's decision margin for that step (the relative
+   distance of a continuous decision from its threshold) is within FP32
+   reach;
+2. whole trajectories of >= 1024 particles per case, recorded step by step:
+   chained single-step launches (state-in from the previous step's FP32
+   outputs) give the reference's edge-id sequence, per-step M and draw counter
+   at every step; a particle may diverge only at a step whose oracle margin
+   is an FP32 near-tie (FP32 state drifts from FP64 by rounding), and the
+   chained run equals ONE multi-step launch bit for bit.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+import golden_io
+import helpers
+import paper_2512_02175_b200 as gs
+from oracle import oracle
+from paper_2512_02175_b200 import engine
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+NEAR_TIE = 2e-5  # decision margin (relative to the terms) an FP32 evaluation can flip
+
+
+def _inj(raw, nrm):
+    return torch.as_tensor(raw.view(np.int64)).to(DEV), torch.as_tensor(nrm).to(DEV)
+
+
+def _cfg(n, dt, cap, refl, n_steps=1, seed=1):
+    return gs.SimulationConfig(dt=float(dt), n_steps=n_steps, n_particles=int(n), seed=seed,
+                               max_splits_per_step=int(cap), reflect_at=float(refl))
+
+
+def _step_rows_native(g, f, d, sel):
+    """Rows ``sel`` of a golden step table through the production kernel, one
+    launch per (dt, cap, wall) group; returns edge, x, M, trunc, draws used."""
+    out = {k: np.zeros(len(d["edge"]), t) for k, t in
+           (("edge", np.int64), ("x", np.float64), ("M", np.int64), ("trunc", np.int64),
+            ("used", np.int64))}
+    for dt, cap, refl in sorted(set(zip(d["dt"][sel].tolist(), d["cap"][sel].tolist(),
+                                        d["refl"][sel].tolist()))):
+        rows = sel[(d["dt"][sel] == dt) & (d["cap"][sel] == cap) & (d["refl"][sel] == refl)]
+        K = 2 * cap + 4
+        raw, nrm = oracle.fill_draws_rows(d["seed"][rows], d["pid"][rows], d["k"][rows], K)
+        state = (torch.as_tensor(d["edge"][rows]), torch.as_tensor(d["x"][rows]))
+        res = engine.ensemble_device(g, f, _cfg(len(rows), dt, cap, refl),
+                                     outputs=("all", "counter"), inject=_inj(raw, nrm),
+                                     precision="native", state=state)
+        assert int(res["totals"][3]) == 0, "a row ran past its injected draws"
+        out["edge"][rows] = res["edge"].cpu().numpy()
+        out["x"][rows] = res["x"].cpu().numpy()
+        out["M"][rows] = res["crossings"].cpu().numpy()
+        out["trunc"][rows] = res["truncs"].cpu().numpy()
+        out["used"][rows] = res["counter"].cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("case", list(cases.CASES))
+def test_golden_steps_through_production_kernel(case):
+    g, f = cases.build(case, gs)
+    d = golden_io.load_npz_groups("steps.npz")[case]
+    n = len(d["edge"])
+    sel = np.arange(n)
+    got = _step_rows_native(g, f, d, sel)
+    sig = f.packed()[5][d["edge"]]
+    used_ref = (d["o_k"] - d["k"]).astype(np.int64)
+    ok_int = ((got["edge"] == d["o_edge"]) & (got["M"] == d["o_M"]) &
+              (got["trunc"] == d["o_trunc"]) & (got["used"] == used_ref))
+    scale = np.maximum.reduce([np.abs(d["x"]), np.abs(d["o_x"]), sig * np.sqrt(d["dt"])])
+    ok_x = np.abs(got["x"] - d["o_x"]) <= 1e-5 * scale
+    bad = np.flatnonzero(~(ok_int & ok_x))
+    if bad.size:  # each disagreement must be a near-tie of the reference's own step
+        og = oracle.OracleGraph(g, f)
+        m = oracle.step_rows(og, d["edge"][bad], d["x"][bad], d["dt"][bad], d["seed"][bad],
+                             d["pid"][bad], d["k"][bad], d["cap"][bad], d["refl"][bad])
+        for j, i in enumerate(bad):
+            print(f"{case} row {i}: ref edge/M/trunc/used {d['o_edge'][i]}/{d['o_M'][i]}/"
+                  f"{d['o_trunc'][i]}/{used_ref[i]} got {got['edge'][i]}/{got['M'][i]}/"
+                  f"{got['trunc'][i]}/{got['used'][i]}; x {d['o_x'][i]!r} vs {got['x'][i]!r}; "
+                  f"FP64 decision margin {m['margin'][j]:.3g}")
+        assert np.all(m["margin"] < NEAR_TIE), m["margin"]
+        assert bad.size <= 2, bad.size  # near-ties are rare (0.5 per 1e4 steps expected)
+    print(f"{case}: {n - bad.size}/{n} rows exact (edge, M, trunc, draws; x within 1e-5)")
+
+
+TRACE_CASES = [  # case, steps, dt, initial law, cap, wall
+    ("star3_bm", 300, 1e-3, ("at", 0), 100, 0.0),         # C1 geometry (driftless kernel)
+    ("star5_quad", 200, 1e-3, ("uniform", 0.4), 100, 0.0),
+    ("star3_drift", 200, 1e-3, ("at", 0), 100, 0.05),     # mirror wall
+    ("star4_mixed", 150, 1e-2, ("uniform", 0.2), 5, 0.0),  # tabulated drift, truncations
+    ("hub64", 200, 1e-3, ("uniform", 2.0), 100, 0.0),      # general, shared-memory tables
+    ("random_general", 150, 2e-3, ("uniform", 1.0), 100, 0.0),
+    ("vascular_small", 150, 1e-3, ("uniform", 2.0), 100, 0.0),  # general, L2 tables
+]
+
+
+@pytest.mark.parametrize("case,steps,dt,init,cap,wall", TRACE_CASES,
+                         ids=[c[0] for c in TRACE_CASES])
+def test_per_step_traces_production_kernel(case, steps, dt, init, cap, wall):
+    g, f = helpers.graph_for(case)
+    n, seed = 1024, 20251202
+    og = oracle.OracleGraph(g, f)
+    ref = oracle.trace(og, seed, n, steps, dt, helpers.oracle_init(init, g), cap, wall)
+    K = 2 * cap + 4
+    pid = np.arange(n, dtype=np.uint64)
+    # step 1 from the configured initial law (placement draws 0, 1 for PerEdgeUniform)
+    cfg1 = gs.SimulationConfig(dt=dt, n_steps=1, n_particles=n, seed=seed, max_splits_per_step=cap,
+                               initial=helpers.initial_for(init), reflect_at=wall)
+    raw, nrm = oracle.fill_draws(seed, n, K + 2)
+    res = engine.ensemble_device(g, f, cfg1, outputs=("all", "counter"), inject=_inj(raw, nrm),
+                                 precision="native")
+    edge_t = np.zeros((n, steps), np.int64)
+    M_t = np.zeros((n, steps), np.int64)
+    k_t = np.zeros((n, steps), np.uint64)
+    x_last = None
+    k = np.zeros(n, np.uint64)
+    for s in range(steps):
+        if s:
+            raw, nrm = oracle.fill_draws_rows(np.full(n, seed, np.uint64), pid, k, K)
+            res = engine.ensemble_device(g, f, _cfg(n, dt, cap, wall, seed=seed),
+                                         outputs=("all", "counter"), inject=_inj(raw, nrm),
+                                         precision="native", state=(res["edge"], res["x"]))
+        assert int(res["totals"][3]) == 0
+        k = k + res["counter"].cpu().numpy().astype(np.uint64)
+        edge_t[:, s] = res["edge"].cpu().numpy()
+        M_t[:, s] = res["crossings"].cpu().numpy()
+        k_t[:, s] = k
+        x_last = res["x"]
+    same = (edge_t == ref["edge"]) & (M_t == ref["M"]) & (k_t == ref["k"])
+    first_bad = np.where(same.all(axis=1), steps, np.argmin(same, axis=1))
+    diverged = np.flatnonzero(first_bad < steps)
+    margins = ref["margin"][diverged, first_bad[diverged]] if diverged.size else np.zeros(0)
+    print(f"{case}: {n - diverged.size}/{n} particles follow the reference's edge ids, M and "
+          f"draw counter at every one of {steps} steps; divergences at FP64 margins "
+          f"{np.sort(margins)[:8]}")
+    assert np.all(margins < NEAR_TIE), margins
+    assert diverged.size <= 0.002 * n + 1, diverged.size
+    # the chained single steps ARE the production run: one multi-step launch
+    # with the same draws gives identical final states, bit for bit
+    Kall = int(ref["k"][:, -1].max()) + K
+    raw, nrm = oracle.fill_draws(seed, n, Kall)
+    cfgS = gs.SimulationConfig(dt=dt, n_steps=steps, n_particles=n, seed=seed,
+                               max_splits_per_step=cap, initial=helpers.initial_for(init),
+                               reflect_at=wall)
+    full = engine.ensemble_device(g, f, cfgS, outputs=("all", "counter"), inject=_inj(raw, nrm),
+                                  precision="native")
+    assert torch.equal(full["edge"], res["edge"])
+    assert torch.equal(full["x"], x_last)
+    np.testing.assert_array_equal(full["crossings"].cpu().numpy(), M_t.sum(axis=1))
+    np.testing.assert_array_equal(full["counter"].cpu().numpy().astype(np.uint64), k)
+
+
+def test_native_resume_from_state_and_counter():
+    """Checkpoint / resume on the native stream: (edge, x, next Philox block)
+    of a run is a complete restart point.  Resuming is deterministic, draws
+    fresh blocks (never re-uses the first run's), and the resumed ensemble is
+    statistically the continuous one (two-sample chi-square on final edges)."""
+    g, f = cases.build("hub8", gs)
+    n = 400_000
+    a = gs.SimulationConfig(dt=1e-2, n_steps=60, n_particles=n, seed=5,
+                            initial=gs.PerEdgeUniform(2.0))
+    first = engine.ensemble_device(g, f, a, outputs=("edge", "x", "counter"))
+    cnt = first["counter"]
+    assert int(cnt.min()) > 0
+    b = gs.SimulationConfig(dt=1e-2, n_steps=60, n_particles=n, seed=5)
+    st = (first["edge"], first["x"], cnt)
+    r1 = engine.ensemble_device(g, f, b, outputs=("edge", "x", "counter", "edge_counts"), state=st)
+    r2 = engine.ensemble_device(g, f, b, outputs=("edge", "x", "counter", "edge_counts"), state=st)
+    for k in ("edge", "x", "counter"):
+        assert torch.equal(r1[k], r2[k]), k
+    assert bool((r1["counter"] > cnt).all())
+    fresh = engine.ensemble_device(g, f, b, outputs=("edge", "x"),
+                                   state=(first["edge"], first["x"]))  # blocks from 0 again
+    assert not torch.equal(fresh["x"], r1["x"])
+    cont = engine.ensemble_device(g, f, gs.SimulationConfig(
+        dt=1e-2, n_steps=120, n_particles=n, seed=6, initial=gs.PerEdgeUniform(2.0)),
+        outputs=("edge_counts",))
+    p, chi2, dof = helpers.chi2_two_sample(r1["edge_counts"].cpu().numpy(),
+                                           cont["edge_counts"].cpu().numpy())
+    assert p > 1e-4, (p, chi2, dof)
+
+
+def test_state_in_rejected_for_reference_stream():
+    g, f = cases.build("hub8", gs)
+    cfg = gs.SimulationConfig(dt=1e-2, n_steps=1, n_particles=4, seed=1, rng="reference")
+    st = (torch.zeros(4, dtype=torch.int32), torch.full((4,), 0.1))
+    with pytest.raises(gs._native.GsdeError):
+        engine.ensemble_device(g, f, cfg, state=st)
