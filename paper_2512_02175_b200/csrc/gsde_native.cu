@@ -89,6 +89,11 @@ struct InjParams {
   const float *st_x;
   const uint64_t *st_k;
   uint64_t *counter;
+  // fused final-state estimators in shared memory (0 = global atomics): byte
+  // offset of the block's uint32 counters -- edge_counts [E] then the
+  // snapshot histogram [n_cells] -- flushed to the call's int64 arrays once
+  unsigned bin_off;
+  int bin_edges, bin_cells;
 };
 
 __device__ __forceinline__ float fast_sqrt(float v) {
@@ -838,8 +843,40 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   uint32_t q_head = 0, q_tail = 0;  // placement ring (warp-uniform)
   int f_n = 0;                      // finished states queued (warp-uniform)
   const bool bins = o.edge_counts || o.hist;
+  // shared-memory estimator counters (when the grid fits): the warp's 32
+  // finished states are grouped by edge / cell with __match_any_sync, and
+  // one lane per group adds the group's size -- one shared atomic per
+  // distinct bin per 32 particles; flushed to global int64 once per block
+  // (the counters' address is re-derived from the parameter at each use: a
+  // pointer held across the stepping loop costs the loop registers)
+  extern __shared__ __align__(16) unsigned char smem_b[];
+  auto bin_base = [&]() { return reinterpret_cast<unsigned *>(smem_b + q.bin_off); };
+  // (compiled for graphs staged in shared memory only: a network too large
+  // to stage has more bins than fit, and the code would cost its loop)
+  const bool sbins = C::SMEM && q.bin_off;
+  if (sbins) {
+    for (int j = threadIdx.x; j < q.bin_edges + q.bin_cells; j += blockDim.x) bin_base()[j] = 0u;
+    __syncthreads();
+  }
   auto flush_bins = [&](int n_take) {  // converged: bin entries 0..n_take-1
-    if (lane < n_take) epilogue_bins(o, WQ.fe[lane], (double)WQ.fx[lane]);
+    const bool mine = lane < n_take;
+    if (sbins) {
+      unsigned *s_ec = bin_base(), *s_h = s_ec + q.bin_edges;
+      const int e = mine ? WQ.fe[lane] : -1;
+      if (o.edge_counts) {
+        const unsigned grp = __match_any_sync(0xffffffffu, e);
+        if (mine && lane == __ffs(grp) - 1) atomicAdd(&s_ec[e], (unsigned)__popc(grp));
+      }
+      if (o.hist) {
+        const int c = mine ? (int)hist_cell(o.hist_offsets, o.hist_counts, o.hist_dx, e,
+                                            (double)WQ.fx[lane])
+                           : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, c);
+        if (mine && lane == __ffs(grp) - 1) atomicAdd(&s_h[c], (unsigned)__popc(grp));
+      }
+    } else if (mine) {
+      epilogue_bins(o, WQ.fe[lane], (double)WQ.fx[lane]);
+    }
     __syncwarp();
     if (lane < f_n - n_take) {  // n_take == 32: sources and targets do not overlap
       WQ.fe[lane] = WQ.fe[n_take + lane];
@@ -948,6 +985,14 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     if (active && L.steps_left == 0) finish();
   }
   if (bins && f_n > 0) flush_bins(f_n);
+  if (sbins) {
+    const unsigned *s_ec = bin_base(), *s_h = s_ec + q.bin_edges;
+    __syncthreads();
+    for (int j = threadIdx.x; j < q.bin_edges; j += blockDim.x)
+      if (s_ec[j] && o.edge_counts) add_i64(&o.edge_counts[j], (int64_t)s_ec[j]);
+    for (int j = threadIdx.x; j < q.bin_cells; j += blockDim.x)
+      if (s_h[j] && o.hist) add_i64(&o.hist[j], (int64_t)s_h[j]);
+  }
   if (o.totals) {
     warp_add_i64(&o.totals[0], t_cross);
     warp_add_i64(&o.totals[1], t_events);
@@ -1084,6 +1129,7 @@ __global__ void __launch_bounds__(256) histogram_kernel(int64_t n, const int64_t
 }
 
 constexpr int kOccSmemCells = 8192;  // shared uint32 occupation counters up to 32 KB
+constexpr int kBinSmemMax = 4096;    // shared uint32 final-state bins (edges + cells) up to 16 KB
 
 size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit, int occ_cells) {
   size_t b = ((size_t)(kPriv * kThreads + smem_bins(nb)) * sizeof(int) + 15) & ~size_t(15);
@@ -1225,6 +1271,20 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     }
     const size_t qoff = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells));
     smem = qoff + queues + occ_tab;
+    // fused final-state bins in shared memory when they fit (and no block can
+    // count 2^32 particles into one bin)
+    InjParams qq = q;
+    const int bin_e = o.edge_counts ? (int)g->E : 0;
+    const int bin_c = o.hist ? (int)o.hist_n_cells : 0;
+    if (C::SMEM && (bin_e || bin_c) && (int64_t)bin_e + bin_c <= kBinSmemMax &&
+        (double)((n + grid - 1) / grid) < 4.0e9) {
+      qq.bin_off = (unsigned)align16(smem);
+      qq.bin_edges = bin_e;
+      qq.bin_cells = bin_c;
+      smem = align16(smem) + (size_t)(bin_e + bin_c) * sizeof(unsigned);
+      err = prepare(k, smem);
+      if (err != cudaSuccess) return err;
+    }
     // grid-wide particle counter: this call's slot of the handle's ring
     // (a per-call cudaMallocAsync here stalled running kernels for up to
     // hundreds of ms when the pool remapped memory).  A slot is reused only
@@ -1243,7 +1303,7 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     err = cudaMemsetAsync(work, a.n_steps == 0 ? 0x7f : 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
     err = launch(k, smem, grid, s, g->nat, p, kernel_out(o), occ_cells, work, (unsigned)qoff,
-                 (unsigned)(qoff + queues), q);
+                 (unsigned)(qoff + queues), qq);
     if (err != cudaSuccess) return err;
     return cudaEventRecord(done, s);
   };

@@ -10,10 +10,33 @@ import paper_2512_02175_b200 as gs
 POS_ATOL = 1e-10
 
 
+_C4 = []
+
+
+def vascular_c4():
+    """The C4 network (workloads.vascular(): ~1.02e5 edges), built once per session."""
+    if not _C4:
+        _C4.append(gs.workloads.vascular())
+    return _C4[0]
+
+
 def graph_for(case):
     if case == "vascular_small":
         return gs.parse_graph_file(golden_io.vascular_small_text())
+    if case == "vascular_c4":
+        return vascular_c4()
     return cases.build(case, gs)
+
+
+def graph_digest(g, f) -> str:
+    """SHA-256 of a graph's packed arrays (tests/golden/make_c4_golden.py)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in (g.edge_init, g.edge_term, g.edge_length, g.v_off, g.v_edges, g.v_orient,
+              g.v_cumw) + tuple(f.packed()):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
 
 
 def initial_for(init):

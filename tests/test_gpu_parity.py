@@ -166,8 +166,10 @@ def test_inject_f32_single_steps_north_star_contract():
             n_rows += sel.size
             n_tie += int((~(ok_int & ok_x)).sum())
     # FP32 vs FP64 can only disagree on decisions within FP32 rounding of a
-    # threshold; over 4800 random steps we allow at most 0.5% such rows.
-    assert n_tie <= 0.005 * n_rows, (n_tie, n_rows)
+    # threshold (the production kernel: 0 of these 4800 rows,
+    # test_gpu_state_parity.py); allow two for the strict-IEEE FP32 stepper
+    print(f"reference-order FP32 stepper: {n_rows - n_tie}/{n_rows} rows exact")
+    assert n_tie <= 2, (n_tie, n_rows)
 
 
 def test_inject_f32_full_trajectories_c1():
@@ -224,10 +226,13 @@ def test_inject_native_kernel_full_trajectories(case, n, steps, dt, init, K, fra
                                                             np.sqrt(dt))
     print(f"{case}: native kernel, injected draws: exact edge+crossings {same.mean():.5f}, "
           f"positions within 1e-5 {close.mean():.5f}")
-    assert same.mean() >= 0.995
+    # measured: 100% of particles (round 1 and 2 runs); allow 1 in 2000 to pass
+    # an FP32 near-tie after its position has drifted (test_gpu_state_parity.py
+    # shows every single step exact)
+    assert same.mean() >= 0.9995
     assert (same & close).mean() >= frac
     loose = np.abs(x - o["positions"]) <= 1e-3 * np.maximum(np.abs(o["positions"]), np.sqrt(dt))
-    assert (same & loose).mean() >= 0.995
+    assert (same & loose).mean() >= 0.999
 
 
 def test_inject_native_kernel_mirror_wall():
@@ -242,7 +247,7 @@ def test_inject_native_kernel_mirror_wall():
     e, c, x = (out[k].cpu().numpy() for k in ("edge", "crossings", "x"))
     same = (e == o["edges"]) & (c == o["crossings"])
     close = np.abs(x - o["positions"]) <= 1e-5 * np.maximum(np.abs(o["positions"]), np.sqrt(dt))
-    assert same.mean() >= 0.995 and (same & close).mean() >= 0.99, (same.mean(), close.mean())
+    assert same.mean() >= 0.9995 and (same & close).mean() >= 0.99, (same.mean(), close.mean())
     assert x.max() <= wall
 
 
@@ -278,8 +283,9 @@ def test_inject_native_trials_kernel(seed):
     same = (M == o["M"]) & (ex == o["exit_edges"]) & (tr == o["truncated"])
     close = np.abs(x - o["exit_positions"]) <= 1e-5 * np.maximum(np.abs(o["exit_positions"]),
                                                                  np.sqrt(dt))
-    assert same.mean() >= 0.995, same.mean()
-    assert (same & close).mean() >= 0.99, (same & close).mean()
+    # a trial is one step from the vertex state: exact up to FP32 near-ties
+    assert same.mean() >= 0.9999, same.mean()
+    assert (same & close).mean() >= 0.999, (same & close).mean()
 
 
 def test_histogram_kernel_matches_oracle():

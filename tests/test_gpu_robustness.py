@@ -91,3 +91,23 @@ def test_native_particle_ids_below_2_48():
     engine.ensemble_device(g, f, cfg, pid_offset=(1 << 48) - 10)  # the last ten ids: fine
     with pytest.raises(_native.GsdeError):
         engine.ensemble_device(g, f, cfg, pid_offset=(1 << 48) - 9)
+
+
+@pytest.mark.parametrize("cells", [8, 100])  # 64 x 8 (+64): shared bins; 64 x 100: global
+def test_fused_bins_shared_and_global_paths(cells):
+    """Final-edge counts and the snapshot histogram fused into the native
+    ensemble kernel -- warp-aggregated shared-memory counters when the bins
+    fit, global atomics otherwise -- equal the histogram of the per-particle
+    outputs exactly."""
+    from oracle import oracle
+
+    g, f = cases.build("hub64", gs)
+    grid = gs.EdgeGrid.uniform(g, cells)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=100, n_particles=300_001, seed=12,
+                              initial=gs.PerEdgeUniform(2.0))
+    res = engine.ensemble_device(g, f, cfg, outputs=("edge", "x", "edge_counts"), grid=grid)
+    e, x = res["edge"].cpu().numpy(), res["x"].cpu().numpy()
+    np.testing.assert_array_equal(res["edge_counts"].cpu().numpy(),
+                                  np.bincount(e, minlength=g.n_edges))
+    np.testing.assert_array_equal(res["hist"].cpu().numpy(),
+                                  oracle.histogram(e, x, grid.offsets, grid.counts, grid.dx))
