@@ -109,7 +109,10 @@ __device__ __forceinline__ float fast_lg2(float v) {
 }
 
 // Box-Muller on two 32-bit words: u1 in (0, 1] with 2^-33 resolution near 0
-// (|z| <= 6.8), angle uniform on [-pi, pi).  Returns z / sqrt(2 ln 2): the
+// (|z| <= sqrt(2 * 33 ln 2) = 6.77), angle uniform on [-pi, pi).  The tail cut
+// drops P(|z| > 6.77) = 1.3e-11 of the Gaussian mass per draw, so any
+// estimator moves by O(1e-11) -- far below the Monte-Carlo resolution of the
+// largest runs here (1e13 psteps: relative SE ~3e-7).  Returns z / sqrt(2 ln 2): the
 // native edge records carry sigma * sqrt(2 ln 2) (gsde_abi.cu), so every
 // sigma * z product is unchanged and the scale costs no instruction here.
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
@@ -210,7 +213,7 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 
 // Compile-time kernel variant.
 template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false,
-          bool INJ_ = false, bool FULL_ = false>
+          bool INJ_ = false, bool FULL_ = false, bool PP_ = true>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
@@ -229,6 +232,14 @@ struct Cfg {
   // register allocation the extra code would otherwise perturb.
   static constexpr bool FULL = FULL_;
   static constexpr bool STATE = FULL_ || INJ_;  // state-in / counter out compiled in
+  // Per-particle counters (crossings, events, truncations per particle) and
+  // the per-particle result arrays.  Off (the "lean" ensemble kernel) when a
+  // call asks only for fused estimators: the run totals then follow from the
+  // M histogram (M <= cap, so crossings = sum b h[b], events = sum_{b>=1} h[b])
+  // plus one shared truncation counter, and the lane carries three
+  // registers and a per-step update less.
+  static constexpr bool PP = PP_;
+  static_assert(PP_ || !(INJ_ || FULL_), "INJ / FULL kernels keep per-particle counters");
   using Cnt = std::conditional_t<FULL_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
 };
@@ -348,16 +359,29 @@ __device__ __forceinline__ void mh_add(const Shared &S, int bin) {
     add_i64(&S.mh_g[bin], 1);
 }
 
-template <bool FULL = false>
+// TOTALS (lean ensemble kernels): the block's crossings and events follow
+// from its M histogram (every bin b <= cap holds steps with exactly M = b),
+// truncations from the shared counter.
+template <bool FULL = false, bool TOTALS = false>
 __device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int occ_cells,
-                             int64_t *occ_out) {
+                             int64_t *occ_out, int64_t *totals = nullptr) {
   __syncthreads();
   const int nbs = FULL ? smem_bins(nb) : nb;
+  int64_t t_cross = 0, t_events = 0;
   for (int b = threadIdx.x; b < nbs; b += blockDim.x) {
     int64_t v = S.mh[b];
     if (b < kPriv)
       for (int t = 0; t < kThreads; ++t) v += S.priv[b * kThreads + t];
     if (v && m_hist) add_i64(&m_hist[b], v);
+    if (TOTALS && b > 0) {
+      t_cross += (int64_t)b * v;
+      t_events += v;
+    }
+  }
+  if (TOTALS && totals) {
+    warp_add_i64(&totals[0], t_cross);
+    warp_add_i64(&totals[1], t_events);
+    if (threadIdx.x == 0 && S.tot[2]) add_i64(&totals[2], (int64_t)S.tot[2]);
   }
   if (S.occ)
     for (int j = threadIdx.x; j < occ_cells; j += blockDim.x)
@@ -450,16 +474,22 @@ struct Lane {
       return (s >= 0.0f && s <= 1.0f) ? 1.0f - s * s : 0.0f;
     }
     const float a = drift(G, px) * dtr;
-    const float s = lo ? split_root(a, b, px) : split_root(-a, -b, len - px);
+    // one root evaluation for either end (selected operands): a divergent
+    // warp would otherwise run both inlined copies
+    const float s = split_root(lo ? a : -a, lo ? b : -b, lo ? px : len - px);
     return 1.0f - s * s;
   }
 
   // macro step finished: statistics, reset for the next step
   __device__ __forceinline__ void step_done(const Shared &S, int cap, float dt, float sqdt) {
     if (M > 0) {
-      cross += M;
-      events += 1;
-      truncs += trunc ? 1 : 0;
+      if constexpr (C::PP) {
+        cross += M;
+        events += 1;
+        truncs += trunc ? 1 : 0;
+      } else if (trunc) {
+        atomicAdd(&S.tot[2], 1ull);  // rare: a step cut at the cap
+      }
       mh_add<C::FULL>(S, M > cap ? cap : M);
     }
     M = 0;
@@ -797,11 +827,13 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   bool queued = false;     // this lane's finished state awaits binning
 
   auto finish = [&]() {
-    t_cross += L.cross;
-    t_events += L.events;
-    t_truncs += L.truncs;
+    if constexpr (C::PP) {
+      t_cross += L.cross;
+      t_events += L.events;
+      t_truncs += L.truncs;
+      epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
+    }
     if (C::INJ) t_over += L.over ? 1 : 0;
-    epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     if (C::STATE && q.counter)  // next block (NATIVE: carry in id's bits 48..) / draws used (INJ)
       q.counter[i] = C::INJ ? (uint64_t)L.k : ((id >> 48) << 32) | blk;
     queued = true;
@@ -816,7 +848,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     while (waiting) {
       id = (uint64_t)(p.id_offset + i);
       place_native(L, G, T, O, p, q, id, star_len);
-      epilogue_particle(o, i, L.e, (double)L.x, 0, 0, 0);
+      if constexpr (C::PP) epilogue_particle(o, i, L.e, (double)L.x, 0, 0, 0);
       epilogue_bins(o, L.e, (double)L.x);
       i += stride;
       waiting = i < p.n;
@@ -993,13 +1025,14 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     for (int j = threadIdx.x; j < q.bin_cells; j += blockDim.x)
       if (s_h[j] && o.hist) add_i64(&o.hist[j], (int64_t)s_h[j]);
   }
-  if (o.totals) {
+  if (o.totals && C::PP) {
     warp_add_i64(&o.totals[0], t_cross);
     warp_add_i64(&o.totals[1], t_events);
     warp_add_i64(&o.totals[2], t_truncs);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush<C::FULL>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ);
+  shared_flush<C::FULL, !C::PP>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ,
+                                o.totals);
 }
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
@@ -1182,7 +1215,7 @@ cudaError_t prepare(K kernel, size_t smem) {
 // Runtime flags -> compile-time kernel variant (Cfg).
 template <bool OCC, class F>
 cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
-                     bool inj = false, bool full = false) {
+                     bool inj = false, bool full = false, bool pp = true) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
@@ -1202,6 +1235,11 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
         if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, true>{});
         return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, true>{})
                   : f(Cfg<ST, SM, false, RF, OCC, false, false, true>{});
+      }
+      if (!pp) {  // lean: fused estimators only
+        if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, false, false>{});
+        return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, false, false>{})
+                  : f(Cfg<ST, SM, false, RF, OCC, false, false, false, false>{});
       }
       if (tab) return f(Cfg<ST, SM, true, RF, OCC>{});
       return zd ? f(Cfg<ST, SM, false, RF, OCC, true>{}) : f(Cfg<ST, SM, false, RF, OCC>{});
@@ -1308,10 +1346,12 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     return cudaEventRecord(done, s);
   };
   const bool full = ensemble_needs_full(a, o);
+  // per-particle counters only when some per-particle array is requested
+  const bool pp = o.edge || o.x || o.crossings || o.events || o.truncs;
   return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
-                              inj, full)
+                              inj, full, pp)
              : dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                               run, inj, full);
+                               run, inj, full, pp);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,

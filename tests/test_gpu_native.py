@@ -196,6 +196,52 @@ def test_native_determinism_and_sharding():
     assert torch.equal(a["m_hist"], parts[0]["m_hist"] + parts[1]["m_hist"])
 
 
+@pytest.mark.parametrize("case", ["star3", "star5", "hub64", "vascular_small", "reflect",
+                                  "tab", "cap3", "occupation"])
+def test_lean_kernel_estimators_equal_per_particle_kernel(case):
+    """The lean ensemble kernel (chosen when no per-particle array is asked
+    for: run totals from the M histogram + a shared truncation counter) and the
+    per-particle kernel run the same streams: every fused estimator must be
+    identical, and the totals must equal the per-particle sums."""
+    cap, kw, occ = 100, {}, None
+    if case == "star3":
+        g, f = workloads.star3()
+        init = gs.AtVertex(0)
+    elif case == "star5":
+        g, f = workloads.star5("linear")
+        init = gs.AtVertex(0)
+    elif case == "reflect":
+        g, f = workloads.star5("quadratic")
+        init, kw = gs.PerEdgeUniform(1.0), {"reflect_at": 1.5}
+    elif case == "vascular_small":
+        g, f = helpers.graph_for("vascular_small")
+        init = gs.PerEdgeUniform(float(g.edge_length.max()))
+    elif case == "tab":
+        g, f = cases.build("star4_mixed", gs)
+        init = gs.AtVertex(0)
+    else:
+        g, f = workloads.hub64()
+        init = gs.PerEdgeUniform(2.0)
+        cap = 3 if case == "cap3" else 100
+        occ = (7, 3) if case == "occupation" else None
+    cfg = gs.SimulationConfig(dt=1e-3 if case != "cap3" else 1e-2, n_steps=300,
+                              n_particles=60_001, seed=5, initial=init,
+                              max_splits_per_step=cap, **kw)
+    grid = gs.EdgeGrid.uniform(g, 4, lengths=[3.0] * g.n_edges if g.is_star else None)
+    lean = engine.ensemble_device(g, f, cfg, outputs=("edge_counts",), grid=grid,
+                                  occupation=occ)
+    pp = engine.ensemble_device(g, f, cfg, outputs=("all", "edge_counts"), grid=grid,
+                                occupation=occ)
+    keys = ("m_hist", "totals", "edge_counts", "hist") + (("occ",) if occ else ())
+    for k in keys:
+        assert torch.equal(lean[k], pp[k]), (case, k, lean[k][:8], pp[k][:8])
+    tot = lean["totals"].cpu().numpy()
+    assert tot[0] == int(pp["crossings"].sum()) and tot[1] == int(pp["events"].sum())
+    assert tot[2] == int(pp["truncs"].sum())
+    if case == "cap3":
+        assert tot[2] > 0  # the truncation counter is exercised
+
+
 @pytest.mark.parametrize("rng", ["native", "reference"])
 def test_full_size_invariants_c1_throughput(rng):
     """C1 throughput size (1.6e7 x 1e3 native; 2e6 x 1e3 reference): the fused
