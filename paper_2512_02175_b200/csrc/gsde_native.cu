@@ -24,11 +24,12 @@
 //  * exit slot: per-vertex alias table, one 16 B column record per pick;
 //  * star / small graphs: edge records and alias columns staged in shared
 //    memory; large networks read them through L2 (__ldg);
-//  * estimators fused: M histogram in lane-private shared counters (M < 8)
-//    + shared atomics; totals in shared memory; occupancy and snapshot
+//  * estimators fused: M histogram in shared counters (one shared atomic
+//    per step with M > 0); totals in shared memory; occupancy and snapshot
 //    histogram in the particle epilogue.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>
@@ -48,8 +49,10 @@ constexpr int kMinBlocksStar = 3;            // star-graph ensembles: <= 85 regi
 // bound; the same kernel scheduled under a 51-register bound (5 blocks) ran 3% slower
 constexpr int kMinBlocksTrials = 4;
 constexpr int kTrialWaves = 4;  // trials grid: resident blocks x 4
-constexpr int kPriv = 8;       // lane-private M-histogram bins
 constexpr int kTrips = 14;     // ensemble: trips per iteration
+#ifndef GSDE_EXIT_PRIV
+#define GSDE_EXIT_PRIV 1  // trials: lane-private exit counters (+0.6% over shared atomics)
+#endif
 constexpr uint32_t kDomainEnsemble = 0u;
 constexpr uint32_t kDomainTrials = 1u;
 constexpr uint32_t kDomainPlace = 0xFFFFFFFFu;
@@ -69,6 +72,12 @@ struct NatParams {
   double init_xmax;
   int32_t start_edge; // trials (general)
   float start_x;
+  // shared 32-bit counters stay exact: each warp of an ensemble block takes
+  // particles only while it has taken fewer than warp_budget (0 = no limit),
+  // and FULL kernels keep only the first mh_smem M bins in shared memory (0
+  // when a block could count 2^32)
+  uint32_t warp_budget;
+  int32_t mh_smem;
 };
 
 // Injected reference draws (Cfg::INJ ensembles): per particle [stride] raw
@@ -272,15 +281,14 @@ struct Occ {
 };
 constexpr int kOccTabEdges = 1024;  // per-edge occupation records staged in shared memory
 
-// Shared block state: lane-private M counters, M histogram, totals, staged
+// Shared block state: M histogram, totals, staged
 // graph, occupation counters.
 struct Shared {
-  int *priv;                 // [kPriv][kThreads]
-  int *mh;                   // [min(cap+1, kMaxSmemBins)]
+  unsigned *mh;              // [min(cap+1, kMaxSmemBins)]
   int nbs;                   // M bins in shared memory (FULL kernels: the rest in mh_g)
-  int64_t *mh_g;             // the call's M histogram (global; FULL kernels)
+  int64_t *mh_g;             // the call's M histogram (global: FULL bins, carries)
   unsigned long long *tot;   // [4]
-  int *exit_priv;            // trials: [E][kThreads] or null
+  unsigned *exit_cnt;        // trials: exit counts [E] (shared atomics) or null
   unsigned *occ;             // [n_cells] or null
 };
 
@@ -293,26 +301,25 @@ __host__ __device__ __forceinline__ int smem_bins(int nb) {
 }
 
 __device__ __forceinline__ size_t shared_head_bytes(int nbs) {
-  return align16((size_t)(kPriv * kThreads + nbs) * sizeof(int)) + 4 * sizeof(unsigned long long);
+  return align16((size_t)nbs * sizeof(int)) + 4 * sizeof(unsigned long long);
 }
 
 // (FULL: the shared M bins are capped at kMaxSmemBins; otherwise the host
 // guarantees cap + 1 <= kMaxSmemBins)
 template <bool STAR, bool SMEM, bool FULL = false>
 __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64_t *m_hist,
-                                             Shared &S, Tables<SMEM> &T, bool exit_priv,
-                                             int occ_cells) {
+                                             Shared &S, Tables<SMEM> &T, bool exit_cnt,
+                                             int occ_cells, int mh_smem = kMaxSmemBins) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int nbs = FULL ? smem_bins(nb) : nb;
-  S.priv = reinterpret_cast<int *>(smem);
-  S.mh = S.priv + kPriv * kThreads;
-  if (FULL) {
-    S.nbs = nbs;
-    S.mh_g = m_hist;
-  }
+  // (FULL: the first mh_smem bins -- 0 when a block could count 2^32 -- in
+  // shared memory, the rest in the call's int64 histogram)
+  const int nbs = FULL ? min(smem_bins(nb), mh_smem) : nb;
+  S.mh = reinterpret_cast<unsigned *>(smem);
+  S.mh_g = m_hist;
+  if (FULL) S.nbs = nbs;
   S.tot = reinterpret_cast<unsigned long long *>(
-      smem + align16((size_t)(kPriv * kThreads + nbs) * sizeof(int)));
-  for (int j = threadIdx.x; j < kPriv * kThreads + nbs; j += blockDim.x) S.priv[j] = 0;
+      smem + align16((size_t)nbs * sizeof(int)));
+  for (int j = threadIdx.x; j < nbs; j += blockDim.x) S.mh[j] = 0u;
   if (threadIdx.x < 4) S.tot[threadIdx.x] = 0ull;
   size_t off = shared_head_bytes(nbs);
   T.edge = G.edge;
@@ -335,11 +342,12 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64
     T.edgev = sv;
     T.col = sc;
   }
-  S.exit_priv = nullptr;
-  if (exit_priv) {
-    S.exit_priv = reinterpret_cast<int *>(smem + off);
-    off += (size_t)G.n_edges * kThreads * sizeof(int);
-    for (int j = threadIdx.x; j < G.n_edges * kThreads; j += blockDim.x) S.exit_priv[j] = 0;
+  S.exit_cnt = nullptr;
+  if (exit_cnt) {
+    S.exit_cnt = reinterpret_cast<unsigned *>(smem + off);
+    off += align16((size_t)G.n_edges * (GSDE_EXIT_PRIV ? kThreads : 1) * sizeof(unsigned));
+    for (int j = threadIdx.x; j < G.n_edges * (GSDE_EXIT_PRIV ? kThreads : 1); j += blockDim.x)
+      S.exit_cnt[j] = 0u;
   }
   S.occ = nullptr;
   if (occ_cells > 0) {
@@ -349,29 +357,30 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64
   __syncthreads();
 }
 
+// One shared atomic per macro step with M > 0 (ATOMS.POPC.INC, no return
+// value).  Measured against lane-private counters for the small bins (the
+// former layout, 8 KB per block, load-add-store with per-lane addressing):
+// +0.4% star3, +1% hub64, +0.8% vascular, +4% C3 trials.  Shared counters are
+// 32-bit: the host bounds what one block can count (per-block particle budget,
+// launch_native_ensemble) and otherwise keeps the bins in global memory
+// (S.nbs = 0); a checked add that carries 2^31 into the int64 arrays cost
+// 2-9% (measured) and was not kept.
 template <bool FULL>
 __device__ __forceinline__ void mh_add(const Shared &S, int bin) {
-  if (bin < kPriv)
-    S.priv[bin * kThreads + threadIdx.x] += 1;
-  else if (!FULL || bin < S.nbs)
-    atomicAdd(&S.mh[bin], 1);
+  if (!FULL || bin < S.nbs)
+    atomicAdd(&S.mh[bin], 1u);
   else if (S.mh_g)
     add_i64(&S.mh_g[bin], 1);
 }
 
-// TOTALS (lean ensemble kernels): the block's crossings and events follow
-// from its M histogram (every bin b <= cap holds steps with exactly M = b),
-// truncations from the shared counter.
 template <bool FULL = false, bool TOTALS = false>
 __device__ void shared_flush(const Shared &S, int nb, int64_t *m_hist, int occ_cells,
                              int64_t *occ_out, int64_t *totals = nullptr) {
   __syncthreads();
-  const int nbs = FULL ? smem_bins(nb) : nb;
+  const int nbs = FULL ? S.nbs : nb;
   int64_t t_cross = 0, t_events = 0;
   for (int b = threadIdx.x; b < nbs; b += blockDim.x) {
-    int64_t v = S.mh[b];
-    if (b < kPriv)
-      for (int t = 0; t < kThreads; ++t) v += S.priv[b * kThreads + t];
+    const int64_t v = S.mh[b];
     if (v && m_hist) add_i64(&m_hist[b], v);
     if (TOTALS && b > 0) {
       t_cross += (int64_t)b * v;
@@ -397,7 +406,9 @@ struct Lane {
   int M;           // vertex resolutions in the current macro step
   bool trunc;
   // a hit whose split time is not yet resolved (pending): star x = -start,
-  // general steps_left < 0 with x = start; its Gaussian pz (a, b re-derived)
+  // general steps_left < 0 with x = start; its Gaussian pz (a, b re-derived).
+  // General ensembles: steps_left < 0 with pz = NaN = at the vertex x, no hit
+  // to resolve (a step that ended there, or a start there)
   float px, pz;
   float mu_a, mu_b, sig, sig_sqdt;  // cached drift / diffusion of e
   float len;       // edge length (star: mirror wall or +inf)
@@ -562,8 +573,12 @@ template <class C>
 __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
                                              const Tables<C::SMEM> &T, const Occ &O,
                                              const NatParams &p, float z, uint32_t u) {
-  if (L.steps_left < 0) {  // pending hit (flag: the step count's sign; x = its start)
-    L.steps_left = -L.steps_left;
+  // at a vertex (flag: the step count's sign): a pending hit -- x its start,
+  // pz its Gaussian -- or, with pz = NaN (ensembles), a step that ended at
+  // the vertex, x the vertex
+  const bool pend = L.steps_left < 0 && !isnan(L.pz);
+  L.steps_left = abs(L.steps_left);
+  if (pend) {
     L.px = L.x;
     // the proposal that overshot, recomputed bit for bit (a hit on the common
     // path had dtr == dt and sq == sqrt(dt)), tells which end it reached
@@ -641,11 +656,15 @@ template <class C, bool SLOT>
 __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
                                      const Tables<C::SMEM> &T, const Shared &S, const Occ &O,
                                      const NatParams &p, float z, uint32_t u) {
-  if constexpr (C::INJ)  // one injected normal per proposal
-    z = (L.steps_left > 0 && L.x > 0.0f && (C::STAR || L.x < L.len)) ? L.inj_gauss() : 0.0f;
-  float xn = fmaf(L.sig_sqdt, z, C::ZD ? L.x : fmaf(L.drift(G, L.x), p.dt, L.x));
+  // star: live lanes with x <= 0 sit at the vertex (x = -start: a pending hit);
+  // general: steps_left > 0 <=> strictly inside the edge (at-vertex lanes carry
+  // steps_left < 0), so the common path tests one integer
   const bool live = L.steps_left > 0;
-  const bool run = live && (L.x > 0.0f) && (C::STAR || L.x < L.len);
+  const bool run = C::STAR ? live && (L.x > 0.0f) : live;
+  const bool vtx = C::STAR ? live && !run : L.steps_left < 0;  // (before this trip's hit)
+  if constexpr (C::INJ)  // one injected normal per proposal
+    z = run ? L.inj_gauss() : 0.0f;
+  float xn = fmaf(L.sig_sqdt, z, C::ZD ? L.x : fmaf(L.drift(G, L.x), p.dt, L.x));
   const bool lo_ok = xn > 0.0f;
   const bool ok = run && lo_ok && (C::STAR || xn < L.len);
   const bool hit = run && !ok;
@@ -657,14 +676,25 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
     else  // general: the flag in the step count's sign, x stays the start
       L.steps_left = -L.steps_left;
   }
-  if (ok) L.x = xn;
+  if (ok) {
+    L.x = xn;
+    L.steps_left -= 1;
+  }
   bool done = ok;
-  if (SLOT && (C::STAR ? live : L.steps_left != 0) && !run) {
-    done = rare_trip<C>(L, G, T, O, p, z, u);
-    if (done) L.step_done(S, p.cap, p.dt, p.sqdt);
+  if (SLOT && vtx) {
+    done = rare_trip<C>(L, G, T, O, p, z, u);  // (general: leaves steps_left >= 0 when done)
+    if (done) {
+      L.step_done(S, p.cap, p.dt, p.sqdt);
+      L.steps_left -= 1;
+      // general: a step that ended at the vertex (residual time used up, or
+      // the cap) starts the next one there: flag it, no hit to resolve
+      if (!C::STAR && L.steps_left > 0 && !(L.x > 0.0f && L.x < L.len)) {
+        L.steps_left = -L.steps_left;
+        L.pz = __int_as_float(0x7fffffff);
+      }
+    }
   }
   if (C::OCC) L.occ_tick(O, done);
-  L.steps_left -= done ? 1 : 0;
   return done;
 }
 
@@ -716,6 +746,10 @@ __device__ __forceinline__ void start_particle(Lane<C> &L, const Tables<C::SMEM>
   L.M = 0;
   L.trunc = false;
   L.steps_left = p.n_steps;
+  if (!C::STAR && !(x > 0.0f && x < L.len)) {  // starts at a vertex (see trip)
+    L.steps_left = -p.n_steps;
+    L.pz = __int_as_float(0x7fffffff);
+  }
   L.cross = L.events = L.truncs = 0;
   L.occ_left = O.start + O.every;
 }
@@ -788,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   Shared S;
   Tables<C::SMEM> T;
   shared_setup<C::STAR, C::SMEM, C::FULL>(G, nb, o.m_hist, S, T, false,
-                                          C::OCC ? occ_smem_cells : 0);
+                                          C::OCC ? occ_smem_cells : 0, p.mh_smem);
   Occ O{o.hist_offsets, o.hist_counts, o.hist_dx, o.occ, S.occ, (int32_t)o.occ_every,
         (int32_t)o.occ_start, nullptr};
   if (C::OCC && G.n_edges <= kOccTabEdges) {
@@ -937,7 +971,11 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
       const int k = __popc(nm);
       if (q_tail - q_head < (uint32_t)k) {  // refill 32 placements
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(work, 32ull);
+        // (a warp past its budget -- q_tail counts the particles it took --
+        // takes nothing more)
+        if (lane == 0)
+          base = (p.warp_budget == 0u || q_tail < p.warp_budget) ? atomicAdd(work, 32ull)
+                                                                 : (unsigned long long)p.n;
         base = __shfl_sync(0xffffffffu, base, 0);
         const int64_t pi = (int64_t)base + lane;
         int e = 0;
@@ -1039,12 +1077,16 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
 // fused exit counts per edge and M histogram including M = 0.
 template <class C, bool OUT>
 __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
-    native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_priv,
+    native_trials_kernel(NativeGraph G, NatParams p, gsde_trials_out o, int exit_cnt,
                          InjParams q) {
+  // HT: run totals from the M histogram (every trial lands in bin M <= cap)
+  // and a shared truncation counter, as in the lean ensemble kernel -- off:
+  // per-lane sums measured 2% faster here (the lane's registers are free)
+  constexpr bool HT = false;
   const int nb = p.cap + 1;
   Shared S;
   Tables<C::SMEM> T;
-  shared_setup<C::STAR, C::SMEM, C::FULL>(G, nb, o.m_hist, S, T, exit_priv != 0, 0);
+  shared_setup<C::STAR, C::SMEM, C::FULL>(G, nb, o.m_hist, S, T, exit_cnt != 0, 0, p.mh_smem);
   const Occ O{};
   const float inf = __int_as_float(0x7f800000);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1085,14 +1127,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
       if (o.x) o.x[i] = (double)L.x;
       if (o.trunc) o.trunc[i] = L.trunc ? 1 : 0;
     }
-    if (S.exit_priv)
-      S.exit_priv[L.e * kThreads + threadIdx.x] += 1;
+    if (S.exit_cnt) {
+#if GSDE_EXIT_PRIV
+      S.exit_cnt[L.e * kThreads + threadIdx.x] += 1;
+#else
+      atomicAdd(&S.exit_cnt[L.e], 1u);
+#endif
+    }
     else if (o.exit_counts)
       add_i64(&o.exit_counts[L.e], 1);
     mh_add<C::FULL>(S, L.M > p.cap ? p.cap : L.M);
-    t_M += L.M;
-    t_ev += L.M > 0 ? 1 : 0;
-    t_tr += L.trunc ? 1 : 0;
+    if constexpr (HT) {
+      if (L.trunc) atomicAdd(&S.tot[2], 1ull);
+    } else {
+      t_M += L.M;
+      t_ev += L.M > 0 ? 1 : 0;
+      t_tr += L.trunc ? 1 : 0;
+    }
     i += stride;
     active = i < p.n;
     if (active) start();
@@ -1117,20 +1168,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
     if (active && !fin) fin = rare_trip<C, false>(L, G, T, O, p, z1, r.w);
     if (fin) finish();
   }
-  if (o.totals) {
+  if (o.totals && !HT) {
     warp_add_i64(&o.totals[0], t_M);
     warp_add_i64(&o.totals[1], t_ev);
     warp_add_i64(&o.totals[2], t_tr);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush<C::FULL>(S, nb, o.m_hist, 0, nullptr);
-  if (S.exit_priv && o.exit_counts) {
+  shared_flush<C::FULL, HT>(S, nb, o.m_hist, 0, nullptr, o.totals);
+  if (S.exit_cnt && o.exit_counts)
     for (int e = threadIdx.x; e < G.n_edges; e += blockDim.x) {
+#if GSDE_EXIT_PRIV
       int64_t v = 0;
-      for (int t = 0; t < kThreads; ++t) v += S.exit_priv[e * kThreads + t];
+      for (int t = 0; t < kThreads; ++t) v += S.exit_cnt[e * kThreads + t];
       if (v) add_i64(&o.exit_counts[e], v);
+#else
+      if (S.exit_cnt[e]) add_i64(&o.exit_counts[e], (int64_t)S.exit_cnt[e]);
+#endif
     }
-  }
 }
 
 // Standalone snapshot histogram (histogram_accumulate): block-private shared
@@ -1164,23 +1218,32 @@ __global__ void __launch_bounds__(256) histogram_kernel(int64_t n, const int64_t
 constexpr int kOccSmemCells = 8192;  // shared uint32 occupation counters up to 32 KB
 constexpr int kBinSmemMax = 4096;    // shared uint32 final-state bins (edges + cells) up to 16 KB
 
-size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool priv_exit, int occ_cells) {
-  size_t b = ((size_t)(kPriv * kThreads + smem_bins(nb)) * sizeof(int) + 15) & ~size_t(15);
+size_t smem_bytes(const gsde_graph *g, int nb, bool stage, bool exit_cnt, int occ_cells) {
+  size_t b = ((size_t)smem_bins(nb) * sizeof(int) + 15) & ~size_t(15);
   b += 4 * sizeof(unsigned long long);
   if (stage) b += (size_t)g->E * (g->is_star ? 16 : 32) + (size_t)g->S * 16;
-  if (priv_exit) b += (size_t)g->E * kThreads * sizeof(int);
+  if (exit_cnt) b += align16((size_t)g->E * (GSDE_EXIT_PRIV ? kThreads : 1) * sizeof(unsigned));
   b += (size_t)occ_cells * sizeof(unsigned);
   return b;
 }
 
 template <class K>
-int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items, int waves = 1) {
+int occupancy_grid(K kernel, size_t smem, int device, int64_t n_items, int waves = 1,
+                   int max_per_sm = 1 << 30) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  if (per_sm > max_per_sm) per_sm = max_per_sm;
   if (per_sm < 1) per_sm = 1;
   const int64_t full = (int64_t)dev_info(device).sm_count * per_sm * waves;
   const int64_t need = (n_items + kThreads - 1) / kThreads;
   return (int)(need < full ? (need < 1 ? 1 : need) : full);
+}
+
+// Testing knob (tests/test_gpu_robustness.py): GSDE_FORCE_GLOBAL_BINS=1 takes
+// the path of runs too large for 32-bit shared counters at any size.
+bool force_global_bins() {
+  static const bool f = std::getenv("GSDE_FORCE_GLOBAL_BINS") != nullptr;
+  return f;
 }
 
 NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
@@ -1196,6 +1259,8 @@ NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t 
   p.cap = cap;
   p.dt = (float)dt;
   p.sqdt = sqrtf((float)dt);
+  p.mh_smem = kMaxSmemBins;
+  p.warp_budget = 0u;
   return p;
 }
 
@@ -1213,7 +1278,8 @@ cudaError_t prepare(K kernel, size_t smem) {
 }
 
 // Runtime flags -> compile-time kernel variant (Cfg).
-template <bool OCC, class F>
+// ENS: ensemble launches (the lean, no-per-particle-counter kernels exist only there)
+template <bool OCC, bool ENS = false, class F>
 cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
                      bool inj = false, bool full = false, bool pp = true) {
   using T = std::true_type;
@@ -1236,10 +1302,12 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
         return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, true>{})
                   : f(Cfg<ST, SM, false, RF, OCC, false, false, true>{});
       }
-      if (!pp) {  // lean: fused estimators only
-        if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, false, false>{});
-        return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, false, false>{})
-                  : f(Cfg<ST, SM, false, RF, OCC, false, false, false, false>{});
+      if constexpr (ENS) {
+        if (!pp) {  // lean: fused estimators only
+          if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, false, false>{});
+          return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, false, false>{})
+                    : f(Cfg<ST, SM, false, RF, OCC, false, false, false, false>{});
+        }
       }
       if (tab) return f(Cfg<ST, SM, true, RF, OCC>{});
       return zd ? f(Cfg<ST, SM, false, RF, OCC, true>{}) : f(Cfg<ST, SM, false, RF, OCC>{});
@@ -1283,6 +1351,17 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   const bool occ = o.occ != nullptr;
   const int d = g->device;
   const int64_t n = a.n_particles;
+  // Shared 32-bit counters (M histogram, occupation, final-state bins) stay
+  // exact: each warp takes at most 4 x its fair share of particles + 64 (the
+  // kernel's warp_budget and its last refill), which bounds what one block
+  // can count -- steps x that for the M histogram / occupation, that for the
+  // final-state bins.  Runs past 2^32 keep those counters in global memory
+  // (FULL kernel, no shared M bins).  (grid >= min(SMs, ceil(n / 256)))
+  const double share = 8.0 * (std::max(256.0, 4.0 * std::ceil((double)n / (8.0 * dev_info(d).sm_count))) + 64.0);
+  const bool big_steps = share * (double)std::max<int64_t>(a.n_steps, 1) >= 4294967295.0 ||
+                         force_global_bins();
+  const bool big_parts = share >= 4294967295.0 || force_global_bins();
+  p.mh_smem = big_steps ? 0 : kMaxSmemBins;
   auto run = [&](auto cfg) -> cudaError_t {
     using C = decltype(cfg);
     // 14-trip iterations; one vertex slot on star graphs (rare, short vertex
@@ -1292,8 +1371,8 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     // on hub64 and vascular.
     constexpr int kSlots = C::STAR ? 1 : 2;
     auto k = native_ensemble_kernel<C, kTrips, kSlots>;
-    // occupation counters in shared memory when the grid is small and no
-    // per-block count can overflow 32 bits
+    // occupation counters in shared memory when the grid is small (shared
+    // counters carry into the int64 arrays, so no run length overflows them)
     int occ_cells = 0;
     if (C::OCC && o.hist_n_cells <= kOccSmemCells) occ_cells = (int)o.hist_n_cells;
     const size_t queues = (kThreads / 32) * kQueueBytesPerWarp;
@@ -1301,21 +1380,21 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     size_t smem = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells)) + queues + occ_tab;
     cudaError_t err = prepare(k, smem);
     if (err != cudaSuccess) return err;
-    const int grid = occupancy_grid(k, smem, d, n);
-    if (occ_cells) {
-      const double per_block = (double)((n + grid - 1) / grid) *
-                               ((double)a.n_steps / (double)(o.occ_every > 0 ? o.occ_every : 1));
-      if (per_block >= 4.0e9) occ_cells = 0;
-    }
+#ifndef GSDE_STAR_BLOCKS
+#define GSDE_STAR_BLOCKS 3
+#endif
+    // star graphs: 3 resident blocks per SM even when the kernel's registers
+    // would allow 4 (24 warps with more registers' worth of ILP each measured
+    // faster)
+    const int grid = occupancy_grid(k, smem, d, n, 1, C::STAR ? GSDE_STAR_BLOCKS : 1 << 30);
+    if (big_steps) occ_cells = 0;
     const size_t qoff = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells));
     smem = qoff + queues + occ_tab;
-    // fused final-state bins in shared memory when they fit (and no block can
-    // count 2^32 particles into one bin)
+    // fused final-state bins in shared memory when they fit
     InjParams qq = q;
     const int bin_e = o.edge_counts ? (int)g->E : 0;
     const int bin_c = o.hist ? (int)o.hist_n_cells : 0;
-    if (C::SMEM && (bin_e || bin_c) && (int64_t)bin_e + bin_c <= kBinSmemMax &&
-        (double)((n + grid - 1) / grid) < 4.0e9) {
+    if (C::SMEM && (bin_e || bin_c) && (int64_t)bin_e + bin_c <= kBinSmemMax && !big_parts) {
       qq.bin_off = (unsigned)align16(smem);
       qq.bin_edges = bin_e;
       qq.bin_cells = bin_c;
@@ -1340,17 +1419,20 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     // (placement-only runs: 0x7f7f... -- past every particle id, nothing handed out)
     err = cudaMemsetAsync(work, a.n_steps == 0 ? 0x7f : 0, sizeof(*work), s);
     if (err != cudaSuccess) return err;
-    err = launch(k, smem, grid, s, g->nat, p, kernel_out(o), occ_cells, work, (unsigned)qoff,
+    NatParams pk = p;  // a warp's budget: 4 x its fair share (+ one refill of 32)
+    const double wb = 4.0 * std::ceil((double)n / ((double)grid * (kThreads / 32))) + 32.0;
+    pk.warp_budget = wb < 4.0e9 ? (uint32_t)wb : 0u;
+    err = launch(k, smem, grid, s, g->nat, pk, kernel_out(o), occ_cells, work, (unsigned)qoff,
                  (unsigned)(qoff + queues), qq);
     if (err != cudaSuccess) return err;
     return cudaEventRecord(done, s);
   };
-  const bool full = ensemble_needs_full(a, o);
+  const bool full = ensemble_needs_full(a, o) || big_steps;
   // per-particle counters only when some per-particle array is requested
   const bool pp = o.edge || o.x || o.crossings || o.events || o.truncs;
-  return occ ? dispatch<true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
+  return occ ? dispatch<true, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
                               inj, full, pp)
-             : dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
+             : dispatch<false, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
                                run, inj, full, pp);
 }
 
@@ -1359,9 +1441,18 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   NatParams p = make_params(a.seed, a.n_trials, a.trial_offset, a.dt, a.cap);
   p.start_edge = (int32_t)a.start_edge;
   p.start_x = (float)a.start_x;
-  const int priv = (o.exit_counts && g->E <= 32) ? 1 : 0;
+  // Trials are assigned grid-stride: a block runs at most ceil(n / (grid x
+  // 256)) x 256 of them, grid >= min(SMs, ceil(n / 256)).  Past 2^32 the
+  // M histogram and exit counts stay in global memory (FULL, no shared bins).
+  const double per_block = std::max(256.0, std::ceil((double)a.n_trials /
+                                                     (dev_info(g->device).sm_count * 256.0)) * 256.0);
+  const bool big = per_block >= 4294967295.0 || force_global_bins();
+  if (big) p.mh_smem = 0;
+  // exit counts in lane-private shared uint32 counters up to 32 edges (shared
+  // atomics: 4096 edges, -0.6%); larger graphs add to the global int64 counts
+  const int exit_cnt = (o.exit_counts && g->E <= (GSDE_EXIT_PRIV ? 32 : 4096) && !big) ? 1 : 0;
   const bool stage = g->nat_graph_smem > 0;
-  const size_t smem = smem_bytes(g, a.cap + 1, stage, priv, 0);
+  const size_t smem = smem_bytes(g, a.cap + 1, stage, exit_cnt, 0);
   const int d = g->device;
   const int64_t n = a.n_trials;
   const bool inj = a.stream == GSDE_STREAM_INJECT;  // (precision GSDE_PREC_NATIVE)
@@ -1371,7 +1462,7 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
   // FULL when a lane's sum of M (<= its trials x cap; conservatively one
   // block per SM) could pass 2^31 or the M histogram outgrows shared memory
   const double per_lane = std::ceil((double)n / ((double)dev_info(d).sm_count * kThreads));
-  const bool full = a.cap + 1 > kMaxSmemBins || per_lane * (double)a.cap >= 2147483647.0;
+  const bool full = a.cap + 1 > kMaxSmemBins || per_lane * (double)a.cap >= 2147483647.0 || big;
   return dispatch<false>(g->is_star, stage, g->has_tab, g->zero_drift, false,
                          [&](auto cfg) -> cudaError_t {
     auto k = out ? native_trials_kernel<decltype(cfg), true>
@@ -1384,7 +1475,7 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
     // waves refill the slots of early blocks (measured: 1 / 2 / 4 / 8 / 16
     // waves 48.8 / 46.8 / 46.0 / 46.0 / 46.4 ms on C3).  A per-lane dynamic
     // hand-out from a warp pool kept 40 registers but cost 7%.
-    return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, priv,
+    return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, exit_cnt,
                   q);
   }, inj, full);
 }

@@ -111,3 +111,54 @@ def test_fused_bins_shared_and_global_paths(cells):
                                   np.bincount(e, minlength=g.n_edges))
     np.testing.assert_array_equal(res["hist"].cpu().numpy(),
                                   oracle.histogram(e, x, grid.offsets, grid.counts, grid.dx))
+
+
+_GLOBAL_BINS_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import analysis, engine, workloads
+out = {{}}
+for name, (g, f), init in (("hub64", workloads.hub64(), gs.PerEdgeUniform(2.0)),
+                           ("star3", workloads.star3(), gs.AtVertex(0))):
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=300, n_particles=200_001, seed=3, initial=init,
+                              max_splits_per_step=4)
+    grid = gs.EdgeGrid.uniform(g, 4, lengths=[3.0] * g.n_edges if g.is_star else None)
+    for lean in (True, False):
+        r = engine.ensemble_device(g, f, cfg, outputs=("edge_counts",) if lean else
+                                   ("all", "edge_counts"), grid=grid, occupation=(3, 1))
+        for k in ("m_hist", "totals", "edge_counts", "hist", "occ"):
+            out[name + ("_lean_" if lean else "_pp_") + k] = r[k].cpu().numpy()
+ec = analysis.vertex_exit_counts(*workloads.star5("linear"), 1e-3, 2_000_001, 4)
+out["trials_counts"], out["trials_m"] = ec.counts, ec.m_histogram
+out["trials_tot"] = np.array([ec.crossings_total, ec.crossing_events, ec.truncation_count])
+np.savez({path!r}, **out)
+"""
+
+
+def test_global_bins_path_equals_shared_counters(tmp_path):
+    """Runs too large for the kernels' 32-bit shared counters (M histogram,
+    occupation, final-state bins, trial exit counts) keep them in global int64
+    memory (FULL kernels, no shared M bins); GSDE_FORCE_GLOBAL_BINS=1 takes that
+    path at a small size.  Every estimator must equal the shared-counter run."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for force in (False, True):
+        path = str(tmp_path / f"bins_{int(force)}.npz")
+        env = dict(os.environ)
+        env.pop("GSDE_FORCE_GLOBAL_BINS", None)
+        if force:
+            env["GSDE_FORCE_GLOBAL_BINS"] = "1"
+        subprocess.run([sys.executable, "-c", _GLOBAL_BINS_SCRIPT.format(root=root, path=path)],
+                       check=True, env=env, timeout=600)
+        res[force] = np.load(path)
+    a, b = res[False], res[True]
+    assert sorted(a.files) == sorted(b.files) and len(a.files) == 23
+    for k in a.files:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    assert a["hub64_lean_m_hist"][4] > 0  # steps at the cap are counted
