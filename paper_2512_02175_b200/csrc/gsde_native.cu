@@ -569,7 +569,9 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
 // Rare trip of a general graph (kernels.py:223-288).  Lanes arrive here at a
 // vertex: first resolve a pending hit (residual time, stop / cap checks),
 // then resample the exit slot and propose from the new edge's endpoint.
-template <class C>
+// VTX: an ensemble lane (a step ending at the vertex flags it at-vertex);
+// vertex trials end there
+template <class C, bool VTX>
 __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
                                              const Tables<C::SMEM> &T, const Occ &O,
                                              const NatParams &p, float z, uint32_t u) {
@@ -585,11 +587,21 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
     const float xn =
         fmaf(L.sig * L.sq, L.pz, C::ZD ? L.px : fmaf(L.drift(G, L.px), L.dtr, L.px));
     L.x = xn <= 0.0f ? 0.0f : L.len;
+    // (an L1 prefetch of the exit column issued here, ahead of the split
+    // math, measured -2.6% on vascular: its address math costs more than the
+    // latency it hides at 32 warps / SM)
     L.M += 1;
     L.dtr = L.split_factor(G) * L.dtr;
-    if (L.dtr <= 0.0f) return true;  // step ends at the vertex, on the old edge
-    if (L.M >= p.cap) {
-      L.trunc = true;
+    // the step ends at the vertex, on the old edge (residual time used up, or
+    // the cap): ensembles start the next step there -- flagged at-vertex, no
+    // hit to resolve: trip()'s decrement leaves -(steps_left - 1)
+    const bool ends = L.dtr <= 0.0f || L.M >= p.cap;
+    if (ends) {
+      L.trunc = L.dtr > 0.0f;
+      if (VTX) {
+        L.steps_left = 2 - L.steps_left;
+        L.pz = __int_as_float(0x7fffffff);
+      }
       return true;
     }
     L.sq = fast_sqrt(L.dtr);
@@ -636,7 +648,7 @@ __device__ __forceinline__ bool rare_trip(Lane<C> &L, const NativeGraph &G,
   if constexpr (C::STAR)
     return rare_star<C, PEND>(L, G, T, O, p, z, u);
   else
-    return rare_general<C>(L, G, T, O, p, z, u);
+    return rare_general<C, PEND>(L, G, T, O, p, z, u);
 }
 
 // One trip for every lane of the warp: lanes with steps left advance; returns
@@ -685,13 +697,7 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
     done = rare_trip<C>(L, G, T, O, p, z, u);  // (general: leaves steps_left >= 0 when done)
     if (done) {
       L.step_done(S, p.cap, p.dt, p.sqdt);
-      L.steps_left -= 1;
-      // general: a step that ended at the vertex (residual time used up, or
-      // the cap) starts the next one there: flag it, no hit to resolve
-      if (!C::STAR && L.steps_left > 0 && !(L.x > 0.0f && L.x < L.len)) {
-        L.steps_left = -L.steps_left;
-        L.pz = __int_as_float(0x7fffffff);
-      }
+      L.steps_left -= 1;  // (general: a step that ended at the vertex leaves it flagged)
     }
   }
   if (C::OCC) L.occ_tick(O, done);
