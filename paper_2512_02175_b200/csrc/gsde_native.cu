@@ -858,7 +858,8 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   // wrap into bits 48.. of the stream-id word -- particle ids stay below 2^48
   // (checked by the host) -- so streams never repeat.
   uint32_t blk = 0;
-  static_assert((NB & (NB - 1)) == 0, "2^32 must be a multiple of the blocks per iteration");
+  static_assert(!C::FULL || (NB & (NB - 1)) == 0,
+                "2^32 must be a multiple of the blocks per iteration");
   uint64_t id = 0;
   int64_t t_cross = 0, t_events = 0, t_truncs = 0, t_over = 0;
   bool waiting = i < p.n;  // next particle not started yet
@@ -1375,8 +1376,13 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     // the next slot).  Measured: (10,1) / (14,1) / (18,1) /
     // (22,1) on star3, (10,2) / (14,2) / (22,2) / (12,3) / (18,3) / (16,4)
     // on hub64 and vascular.
-    constexpr int kSlots = C::STAR ? 1 : 2;
-    auto k = native_ensemble_kernel<C, kTrips, kSlots>;
+#ifndef GSDE_GQ
+#define GSDE_GQ 14
+#define GSDE_GS 2
+#endif
+    constexpr int kSlots = C::STAR ? 1 : ((C::FULL || C::INJ) ? 2 : GSDE_GS);
+    constexpr int kQ = C::STAR ? kTrips : ((C::FULL || C::INJ) ? kTrips : GSDE_GQ);
+    auto k = native_ensemble_kernel<C, kQ, kSlots>;
     // occupation counters in shared memory when the grid is small (shared
     // counters carry into the int64 arrays, so no run length overflows them)
     int occ_cells = 0;

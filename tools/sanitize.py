@@ -17,6 +17,8 @@ for case, init in (("star3_bm", gs.AtVertex(0)), ("hub8", gs.PerEdgeUniform(2.0)
                                   initial=init)
         engine.ensemble_device(g, f, cfg, outputs=("all", "edge_counts"), grid=grid,
                                occupation=(1, 5))
+        # the lean kernel (fused estimators only)
+        engine.ensemble_device(g, f, cfg, outputs=("edge_counts",), grid=grid)
     if g.is_star or not g.has_semi_infinite_edges:
         for rng in ("native", "reference"):
             engine.trials_device(g, f, 1e-3, 5000, 3, rng=rng)
