@@ -1393,11 +1393,10 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
     cudaError_t err = prepare(k, smem);
     if (err != cudaSuccess) return err;
 #ifndef GSDE_STAR_BLOCKS
-#define GSDE_STAR_BLOCKS 3
+#define GSDE_STAR_BLOCKS (1 << 30)
 #endif
-    // star graphs: 3 resident blocks per SM even when the kernel's registers
-    // would allow 4 (24 warps with more registers' worth of ILP each measured
-    // faster)
+    // (GSDE_STAR_BLOCKS caps star grids per SM for experiments: 3 vs 4 resident
+    // blocks of the 61-register driftless star kernel measured -0.3%)
     const int grid = occupancy_grid(k, smem, d, n, 1, C::STAR ? GSDE_STAR_BLOCKS : 1 << 30);
     if (big_steps) occ_cells = 0;
     const size_t qoff = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells));
