@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -64,11 +66,16 @@ int cuda_fail(cudaError_t e, const char *what) {
 
 // Vose alias table over one vertex's slot weights: column j keeps slot j
 // with probability prob[j], else jumps to alias[j].
+// (scratch vectors reused across vertices: a 1e5-vertex network otherwise
+// spends its graph upload in the allocator)
 void build_alias(const double *w, int deg, std::vector<double> &prob, std::vector<int> &alias) {
+  static thread_local std::vector<double> p;
+  static thread_local std::vector<int> small, large;
   prob.assign(deg, 1.0);
   alias.resize(deg);
-  std::vector<double> p(deg);
-  std::vector<int> small, large;
+  p.resize(deg);
+  small.clear();
+  large.clear();
   double tot = 0.0;
   for (int j = 0; j < deg; ++j) tot += w[j];
   for (int j = 0; j < deg; ++j) {
@@ -128,15 +135,45 @@ ArenaPool &arena_pool() {
 
 size_t g_is_general_size(int32_t is_star, int64_t S) { return is_star ? 0 : (size_t)S * 5; }
 
-struct Arena {
-  std::vector<unsigned char> host;
-  size_t add(const void *src, size_t bytes) {
-    const size_t off = (host.size() + 255) & ~size_t(255);
-    host.resize(off + (bytes ? bytes : 1));
-    if (bytes) memcpy(host.data() + off, src, bytes);
+// Device-arena layout: 256-byte aligned slices, sizes known up front, so the
+// packing loops write straight into the upload buffer.
+struct Layout {
+  size_t size = 0;
+  size_t add(size_t bytes) {
+    const size_t off = (size + 255) & ~size_t(255);
+    size = off + (bytes ? bytes : 1);
     return off;
   }
 };
+
+// Process-wide pinned staging buffer for graph uploads, grown on demand and
+// kept: every graph_create packs into warm, page-locked memory (a 1e5-edge
+// network spent ~30 ms of its upload in first-touch page faults of fresh
+// host vectors, and the copy from pageable memory ran at ~5 GB/s).
+struct Staging {
+  std::mutex mu;
+  unsigned char *buf = nullptr;
+  size_t cap = 0;
+  unsigned char *get(size_t bytes) {  // caller holds mu
+    if (bytes > cap) {
+      if (buf) cudaFreeHost(buf);
+      buf = nullptr;
+      cap = 0;
+      const size_t want = bytes + bytes / 4;
+      if (cudaHostAlloc(&buf, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        buf = nullptr;
+        return nullptr;
+      }
+      cap = want;
+    }
+    return buf;
+  }
+};
+Staging &staging() {
+  static Staging *s = new Staging();  // never destroyed
+  return *s;
+}
 
 }  // namespace
 }  // namespace gsde
@@ -183,12 +220,52 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   DeviceGuard guard(device);
   if (!guard.ok) return set_error(GSDE_ENODEV, "graph_create: cannot select device %d", device);
 
-  // --- host-side packing --------------------------------------------------
-  std::vector<int32_t> einit(E), eterm(E), voff(V + 1), vedges(S), taboff(E + 1);
-  std::vector<uint8_t> vorient(S), kind(E);
-  std::vector<uint64_t> thresh(S);
-  std::vector<double> len64(E), coef64(E), sig64(E), tabx64(T ? T : 1), tabmu64(T ? T : 1);
-  std::vector<float> len32(E), coef32(E), sig32(E), tabx32(T ? T : 1), tabmu32(T ? T : 1);
+  static const bool timing = std::getenv("GSDE_TIMING") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto lap = [&](const char *what) {
+    if (!timing) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gsde] graph_create %s: %.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t_start).count());
+    t_start = t;
+  };
+  // --- layout of the device arena ----------------------------------------
+  const int64_t T1 = T ? T : 1;
+  const size_t nfat = g_is_general_size(d->is_star, S);
+  Layout Lo;
+  const size_t o_len64 = Lo.add(E * 8), o_coef64 = Lo.add(E * 8), o_sig64 = Lo.add(E * 8),
+               o_tabx64 = Lo.add(T1 * 8), o_tabmu64 = Lo.add(T1 * 8), o_len32 = Lo.add(E * 4),
+               o_coef32 = Lo.add(E * 4), o_sig32 = Lo.add(E * 4), o_tabx32 = Lo.add(T1 * 4),
+               o_tabmu32 = Lo.add(T1 * 4), o_einit = Lo.add(E * 4), o_eterm = Lo.add(E * 4),
+               o_voff = Lo.add((V + 1) * 4), o_vedges = Lo.add(S * 4), o_vorient = Lo.add(S),
+               o_thresh = Lo.add(S * 8), o_kind = Lo.add(E), o_taboff = Lo.add((E + 1) * 4),
+               o_nedge = Lo.add(E * sizeof(float4)), o_nedgev = Lo.add(E * sizeof(int4)),
+               o_ncol = Lo.add(S * sizeof(int4)), o_nfat = Lo.add(nfat * sizeof(int4)),
+               o_work = Lo.add(gsde_graph::kWorkSlots * sizeof(unsigned long long));
+  Staging &st = staging();
+  std::lock_guard<std::mutex> staging_lock(st.mu);
+  unsigned char *H = st.get(Lo.size);
+  if (!H) return set_error(GSDE_ENOMEM, "graph_create: cudaHostAlloc(%zu) failed", Lo.size);
+  auto at = [&](size_t off, auto *type) { return reinterpret_cast<decltype(type)>(H + off); };
+  double *len64 = at(o_len64, (double *)0), *coef64 = at(o_coef64, (double *)0),
+         *sig64 = at(o_sig64, (double *)0), *tabx64 = at(o_tabx64, (double *)0),
+         *tabmu64 = at(o_tabmu64, (double *)0);
+  float *len32 = at(o_len32, (float *)0), *coef32 = at(o_coef32, (float *)0),
+        *sig32 = at(o_sig32, (float *)0), *tabx32 = at(o_tabx32, (float *)0),
+        *tabmu32 = at(o_tabmu32, (float *)0);
+  int32_t *einit = at(o_einit, (int32_t *)0), *eterm = at(o_eterm, (int32_t *)0),
+          *voff = at(o_voff, (int32_t *)0), *vedges = at(o_vedges, (int32_t *)0),
+          *taboff = at(o_taboff, (int32_t *)0);
+  uint8_t *vorient = at(o_vorient, (uint8_t *)0), *kind = at(o_kind, (uint8_t *)0);
+  uint64_t *thresh = at(o_thresh, (uint64_t *)0);
+  float4 *nedge = at(o_nedge, (float4 *)0);
+  int4 *nedgev = at(o_nedgev, (int4 *)0), *ncol = at(o_ncol, (int4 *)0),
+       *nfat4 = at(o_nfat, (int4 *)0);
+  memset(at(o_work, (unsigned char *)0), 0, gsde_graph::kWorkSlots * sizeof(unsigned long long));
+  tabx64[0] = tabmu64[0] = 0.0;
+  tabx32[0] = tabmu32[0] = 0.0f;
+
+  // --- host-side packing (into the pinned staging buffer) -----------------
   bool has_tab = false, zero_drift = true;
   for (int64_t e = 0; e < E; ++e) {
     einit[e] = (int32_t)d->edge_init[e];
@@ -223,8 +300,6 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     thresh[j] = (uint64_t)c;
   }
   // native records
-  std::vector<float4> nedge(E);
-  std::vector<int4> nedgev(E), ncol(S);
   for (int64_t e = 0; e < E; ++e) {
     float4 r;
     // FP32 length rounded toward zero, so every native position (<= the FP32
@@ -270,9 +345,8 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
       ncol[sp] = c;
     }
   }
-
+  lap("records + alias tables");
   // fat alias columns for general graphs (one L2 round trip per vertex event)
-  std::vector<int4> nfat(g_is_general_size(d->is_star, S));
   if (!d->is_star) {
     for (int64_t j = 0; j < S; ++j) {
       const int4 c = ncol[j];
@@ -280,43 +354,28 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
       int4 pe4, ae4;
       memcpy(&pe4, &nedge[pe], sizeof(int4));
       memcpy(&ae4, &nedge[ae], sizeof(int4));
-      nfat[5 * j + 0] = c;
-      nfat[5 * j + 1] = pe4;
-      nfat[5 * j + 2] = nedgev[pe];
-      nfat[5 * j + 3] = ae4;
-      nfat[5 * j + 4] = nedgev[ae];
+      nfat4[5 * j + 0] = c;
+      nfat4[5 * j + 1] = pe4;
+      nfat4[5 * j + 2] = nedgev[pe];
+      nfat4[5 * j + 3] = ae4;
+      nfat4[5 * j + 4] = nedgev[ae];
     }
   }
-  Arena A;
-  const size_t o_len64 = A.add(len64.data(), E * 8), o_coef64 = A.add(coef64.data(), E * 8),
-               o_sig64 = A.add(sig64.data(), E * 8), o_tabx64 = A.add(tabx64.data(), tabx64.size() * 8),
-               o_tabmu64 = A.add(tabmu64.data(), tabmu64.size() * 8),
-               o_len32 = A.add(len32.data(), E * 4), o_coef32 = A.add(coef32.data(), E * 4),
-               o_sig32 = A.add(sig32.data(), E * 4), o_tabx32 = A.add(tabx32.data(), tabx32.size() * 4),
-               o_tabmu32 = A.add(tabmu32.data(), tabmu32.size() * 4),
-               o_einit = A.add(einit.data(), E * 4), o_eterm = A.add(eterm.data(), E * 4),
-               o_voff = A.add(voff.data(), (V + 1) * 4), o_vedges = A.add(vedges.data(), S * 4),
-               o_vorient = A.add(vorient.data(), S), o_thresh = A.add(thresh.data(), S * 8),
-               o_kind = A.add(kind.data(), E), o_taboff = A.add(taboff.data(), (E + 1) * 4),
-               o_nedge = A.add(nedge.data(), E * sizeof(float4)),
-               o_nedgev = A.add(nedgev.data(), E * sizeof(int4)),
-               o_ncol = A.add(ncol.data(), S * sizeof(int4)),
-               o_nfat = A.add(nfat.data(), nfat.size() * sizeof(int4));
-  const std::vector<unsigned long long> work(gsde_graph::kWorkSlots, 0ull);
-  const size_t o_work = A.add(work.data(), work.size() * sizeof(unsigned long long));
-  size_t arena_bytes = A.host.size();
-  void *dev = arena_pool().take(device, A.host.size(), &arena_bytes);
+  lap("fat columns");
+  size_t arena_bytes = Lo.size;
+  void *dev = arena_pool().take(device, Lo.size, &arena_bytes);
   cudaError_t err = cudaSuccess;
   if (!dev) {
-    err = cudaMalloc(&dev, A.host.size());
+    err = cudaMalloc(&dev, Lo.size);
     if (err != cudaSuccess) return set_error(GSDE_ENOMEM, "graph_create: cudaMalloc(%zu): %s",
-                                             A.host.size(), cudaGetErrorString(err));
+                                             Lo.size, cudaGetErrorString(err));
   }
-  err = cudaMemcpy(dev, A.host.data(), A.host.size(), cudaMemcpyHostToDevice);
+  err = cudaMemcpy(dev, H, Lo.size, cudaMemcpyHostToDevice);
   if (err != cudaSuccess) {
     cudaFree(dev);
     return cuda_fail(err, "graph_create: upload");
   }
+  lap("device arena + upload");
   auto P = [&](size_t off) { return (void *)((unsigned char *)dev + off); };
   gsde_graph *g = new gsde_graph();
   g->device = device;
