@@ -355,14 +355,23 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
 #: about geometrically (each copy still hides behind the next kernel: D2H moves
 #: a chunk ~2.7x faster than the kernel makes it), so the exposed copy of the
 #: last one is small.  C1 run_ensemble: (0.4, 0.3, 0.2, 0.1) 26.6 ms, these 25.9.
+# Chunk schedules (fractions of the particle ids).  Kernel-bound runs (a
+# particle's steps take longer than its 32 B of D2H at ~55 GB/s: roughly
+# n_steps >= 256 at 3-7e11 psteps/s) want a large first chunk and a small last
+# one (the copies hide under the next kernels); transfer-bound runs want a
+# small first chunk, so the copy engine starts early.  Measured (ms per
+# run_ensemble, one B200): star3 1.6e7 x 1000: 25.5 (kernel-bound schedule) vs
+# 26.0; hub64 1e8 x 1000: 267.2 vs 268.2; vascular 1e8 x 100: 88.9 vs 76.7.
 _CHUNKS = (0.5, 0.28, 0.14, 0.06, 0.02)
+_CHUNKS_TRANSFER_BOUND = (0.08, 0.22, 0.3, 0.25, 0.12, 0.03)
 _PIPELINE_MIN = 1 << 22
 _COPY_STREAMS: dict = {}  # device -> (copy stream, second launch stream)
 
 
-def _chunk_bounds(n: int) -> np.ndarray:
+def _chunk_bounds(n: int, n_steps: int = 1000) -> np.ndarray:
     """Particle-id boundaries of run_ensemble's chunks: [0, ..., n]."""
-    bounds = np.concatenate([[0], np.cumsum(np.floor(np.array(_CHUNKS) * n).astype(np.int64))])
+    fr = _CHUNKS if n_steps >= 256 else _CHUNKS_TRANSFER_BOUND
+    bounds = np.concatenate([[0], np.cumsum(np.floor(np.array(fr) * n).astype(np.int64))])
     bounds[-1] = n
     return bounds
 
@@ -402,7 +411,7 @@ def _ensemble_to_host(graph, field, config, pid_offset=0, n_particles=None, grid
     side.wait_stream(compute)  # whatever the caller queued comes first
     hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
              for k in names]
-    bounds = _chunk_bounds(n)
+    bounds = _chunk_bounds(n, config.n_steps)
     parts = []
     for c, (lo, hi) in enumerate(zip(bounds[:-1], bounds[1:])):
         if hi <= lo:
