@@ -229,9 +229,12 @@ def _pack(graph: MetricGraph, field: CoefficientField, grid: EdgeGrid) -> _Packe
     v_cells = np.where(at_init, offs[ve], offs[ve + 1] - 1).astype(np.int64)
     x_v = np.where(at_init, 0.0, np.asarray(grid.lengths, np.float64)[ve])
     mu_v = np.empty(ve.shape[0])
-    for e in np.unique(ve):
-        sel = ve == e
-        mu_v[sel] = _drift_at(field, int(e), x_v[sel])
+    # group the slots by edge (one _drift_at call per edge, same values as the
+    # reference's per-slot evaluation; a mask per edge made this O(E x S))
+    order = np.argsort(ve, kind="stable")
+    u_e, first = np.unique(ve[order], return_index=True)
+    for e, idx in zip(u_e.tolist(), np.split(order, first[1:])):
+        mu_v[idx] = _drift_at(field, int(e), x_v[idx])
     speed = np.where(at_init, -mu_v, mu_v)
     v_speed_in = np.where(speed > 0.0, speed, 0.0)
     v_D = 0.5 * sig[ve] ** 2
