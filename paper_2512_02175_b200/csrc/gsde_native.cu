@@ -248,6 +248,9 @@ struct Cfg {
   // plus one shared truncation counter, and the lane carries three
   // registers and a per-step update less.
   static constexpr bool PP = PP_;
+  // run totals from the block's M histogram + the shared truncation counter
+  // (every kernel but FULL -- global M bins -- and INJ -- overrun counts)
+  static constexpr bool HT = !FULL_ && !INJ_;
   static_assert(PP_ || !(INJ_ || FULL_), "INJ / FULL kernels keep per-particle counters");
   using Cnt = std::conditional_t<FULL_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
@@ -498,9 +501,8 @@ struct Lane {
         cross += M;
         events += 1;
         truncs += trunc ? 1 : 0;
-      } else if (trunc) {
-        atomicAdd(&S.tot[2], 1ull);  // rare: a step cut at the cap
       }
+      if (C::HT && trunc) atomicAdd(&S.tot[2], 1ull);  // rare: a step cut at the cap
       mh_add<C::FULL>(S, M > cap ? cap : M);
     }
     M = 0;
@@ -869,9 +871,11 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
 
   auto finish = [&]() {
     if constexpr (C::PP) {
-      t_cross += L.cross;
-      t_events += L.events;
-      t_truncs += L.truncs;
+      if (!C::HT) {
+        t_cross += L.cross;
+        t_events += L.events;
+        t_truncs += L.truncs;
+      }
       epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     }
     if (C::INJ) t_over += L.over ? 1 : 0;
@@ -1070,14 +1074,14 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     for (int j = threadIdx.x; j < q.bin_cells; j += blockDim.x)
       if (s_h[j] && o.hist) add_i64(&o.hist[j], (int64_t)s_h[j]);
   }
-  if (o.totals && C::PP) {
+  if (o.totals && !C::HT) {
     warp_add_i64(&o.totals[0], t_cross);
     warp_add_i64(&o.totals[1], t_events);
     warp_add_i64(&o.totals[2], t_truncs);
     if (C::INJ) warp_add_i64(&o.totals[3], t_over);
   }
-  shared_flush<C::FULL, !C::PP>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ,
-                                o.totals);
+  shared_flush<C::FULL, C::HT>(S, nb, o.m_hist, C::OCC ? occ_smem_cells : 0, o.occ,
+                               o.totals);
 }
 
 // Vertex trials: one macro step per trial from the vertex (kernels.py:447-521),
@@ -1107,7 +1111,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   int32_t t_ev = 0, t_tr = 0, t_over = 0;
   auto start = [&]() {
     id = (uint64_t)(p.id_offset + i);
-    L.load_edge(T, O, C::STAR ? 0 : p.start_edge, p.sqdt, inf);
+    // (star: every trial's first trip picks its exit edge, which loads that
+    // edge's record, so the start needs none; general: the start edge's
+    // endpoint record names the vertex's slots)
+    if (!C::STAR) L.load_edge(T, O, p.start_edge, p.sqdt, inf);
     L.x = C::STAR ? 0.0f : p.start_x;
     L.dtr = p.dt;
     L.sq = p.sqdt;
