@@ -319,6 +319,15 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
       memcpy(&r.y, &off, sizeof(float));
       r.z = NAN;
     }
+    if (d->is_star) {
+      // star edges are semi-infinite: the x slot carries sig^2 / mu(0)^2 of the
+      // native record (the failed-excursion time per w^2; constant drift mu0 =
+      // the coefficient, linear mu0 = 0 -> inf; tabulated drifts keep the
+      // generic formula in their kernel)
+      const double mu0 = kind[e] == 0 ? (double)r.y : 0.0;
+      r.x = kind[e] == 2 ? NAN
+            : (mu0 != 0.0 ? (float)(((double)r.w * r.w) / (mu0 * mu0)) : INFINITY);
+    }
     nedge[e] = r;
     const int32_t a = einit[e], b = eterm[e];
     nedgev[e] = make_int4(voff[a], voff[a + 1] - voff[a], b >= 0 ? voff[b] : 0,

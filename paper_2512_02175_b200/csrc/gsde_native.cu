@@ -415,6 +415,7 @@ struct Lane {
   float px, pz;
   float mu_a, mu_b, sig, sig_sqdt;  // cached drift / diffusion of e
   float len;       // edge length (star: mirror wall or +inf)
+  float kex;       // star: sig^2 / mu(0)^2 of e (the failed-excursion time, per w^2)
   int4 ev;         // endpoint alias info of e (general graphs)
   int steps_left;
   typename C::Cnt cross, events, truncs;
@@ -451,6 +452,7 @@ struct Lane {
     sig_sqdt = r.w * sqdt;
     if (C::STAR) {
       len = star_len;
+      kex = r.x;  // star records: sig^2 / mu(0)^2 (gsde_abi.cu), read by rare_star
     } else {
       len = r.x;
       ev = T.V(e2);
@@ -556,8 +558,15 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
     L.x = (C::REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
     return true;
   }
-  const float alpha = (w * w * L.sig * L.sig) * fast_rcp(mu0 * mu0 * L.dtr);
-  L.dtr = (1.0f - alpha) * L.dtr;
+  // failed excursion: dt' = (1 - alpha) dt with alpha = w^2 sig^2 / (mu0^2 dt)
+  // (kernels.py:210-212), i.e. dt' = dt - w^2 sig^2 / mu0^2 -- one FFMA with the
+  // edge's sig^2 / mu0^2 from its record (tabulated drifts: mu0 from the table)
+  if constexpr (C::TAB) {
+    const float alpha = (w * w * L.sig * L.sig) * fast_rcp(mu0 * mu0 * L.dtr);
+    L.dtr = (1.0f - alpha) * L.dtr;
+  } else {
+    L.dtr = fmaf(-(w * w), L.kex, L.dtr);
+  }
   L.x = 0.0f;
   if (L.dtr <= 0.0f) return true;
   if (L.M >= p.cap) {
@@ -709,7 +718,7 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
 // Initial state of particle id (kernels.py:291-307, engine.py:194-203): the
 // edge and position only.
 // PerEdgeUniform from two raw 64-bit draws (kernels.py:298-305)
-template <bool SMEM>
+template <bool SMEM, bool STAR>
 __device__ __forceinline__ void place_from_raw(const NativeGraph &G, const Tables<SMEM> &T,
                                                const NatParams &p, uint64_t r0, uint64_t r1,
                                                int &e, float &x) {
@@ -717,7 +726,8 @@ __device__ __forceinline__ void place_from_raw(const NativeGraph &G, const Table
   const double u2 = (double)(r1 >> 11) * kInv2p53;
   e = (int)(u * (double)G.n_edges);
   if (e >= G.n_edges) e = G.n_edges - 1;
-  const double le = (double)T.E(e).x;
+  // (star edges are semi-infinite; their records' x slot holds sig^2 / mu0^2)
+  const double le = STAR ? (double)INFINITY : (double)T.E(e).x;
   x = (float)(u2 * (le < p.init_xmax ? le : p.init_xmax));
 }
 
@@ -729,16 +739,16 @@ __device__ __forceinline__ void place_values(const NativeGraph &G, const Tables<
                                              int &e, float &x) {
   if (p.init_kind == GSDE_INIT_POINT) {
     e = p.init_edge;
-    x = fminf(p.init_x, T.E(e).x);  // the FP32 edge, like every native position
+    x = C::STAR ? p.init_x : fminf(p.init_x, T.E(e).x);  // the FP32 edge, like every position
   } else if (C::STATE && p.init_kind == GSDE_INIT_STATE) {
     e = __ldg(q.st_e + i);  // coalesced: a warp refills 32 consecutive ids
     x = __ldg(q.st_x + i);
   } else if constexpr (C::INJ) {
     const uint64_t *r = q.raw + i * q.stride;
-    place_from_raw<C::SMEM>(G, T, p, __ldg(r), __ldg(r + 1), e, x);
+    place_from_raw<C::SMEM, C::STAR>(G, T, p, __ldg(r), __ldg(r + 1), e, x);
   } else {
     const Block r = native_block(p, 0u, kDomainPlace, (uint64_t)(p.id_offset + i));
-    place_from_raw<C::SMEM>(G, T, p, ((uint64_t)r.x << 32) | r.y, ((uint64_t)r.z << 32) | r.w,
+    place_from_raw<C::SMEM, C::STAR>(G, T, p, ((uint64_t)r.x << 32) | r.y, ((uint64_t)r.z << 32) | r.w,
                             e, x);
   }
 }
