@@ -552,7 +552,7 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
     L.load_edge(T, O, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
   }
   const float w = fabsf(z);
-  const float mu0 = L.drift(G, 0.0f);
+  const float mu0 = C::TAB ? L.drift(G, 0.0f) : L.mu_a;  // mu(0) = mu_a (+ mu_b * 0)
   const float xn = C::ZD ? (L.sig * L.sq) * w : fmaf(L.sig * L.sq, w, mu0 * L.dtr);
   if (C::ZD || xn >= 0.0f) {
     L.x = (C::REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
