@@ -77,3 +77,24 @@ def test_product_path_fails_loudly_without_gpu():
     with pytest.raises(_native.NativeUnavailable):
         gs.analysis.histogram_accumulate(np.zeros(2, np.int64), np.zeros(2),
                                          gs.EdgeGrid.uniform(g, 2, lengths=[1.0] * 3))
+
+
+def test_integration_stub_structs_match_the_abi():
+    """The ctypes stub in INTEGRATION.md (what a reference maintainer would paste)
+    declares every field of gsde_graph_desc / gsde_run / gsde_out, in order."""
+    import ast
+    import os
+    import re
+
+    from paper_2512_02175_b200 import _native
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    for stub, ours in (("GraphDesc", _native.GraphDesc), ("Run", _native.Run),
+                       ("Out", _native.Out)):
+        m = re.search(r"class %s\(C\.Structure\):\s*_fields_ = (\[.*?\])[ \t]*(?:#[^\n]*)?\n"
+                      % stub, text, re.S)
+        assert m, stub
+        src = re.sub(r"#[^\n]*", "", m.group(1))
+        names = [n for n, _ in ast.literal_eval(re.sub(r"\b(P|i64|u64|f64|i32)\b", "0", src))]
+        assert names == [f[0] for f in ours._fields_], stub
