@@ -534,11 +534,34 @@ struct Lane {
 // vertex (x == 0, possibly with an unresolved overshoot from an earlier trip)
 // or beyond the optional mirror wall.  Returns true when the macro step
 // completed.
+#ifndef GSDE_STAR_NEG
+#define GSDE_STAR_NEG 0  // measured: star3 -4.7% (the at-vertex flagging costs the region more than the trips save)
+#endif
+// Star ensembles (PEND): like general graphs, a lane at the vertex carries a
+// negative step count -- a pending hit (x its start point, pz its Gaussian) or,
+// with pz = NaN, a lane waiting there (a failed excursion, or a step that
+// ended at the vertex) -- so the common trip tests one integer.
+template <class C>
+__device__ __forceinline__ void flag_at_vertex(Lane<C> &L, bool step_done) {
+  // (step_done: trip()'s decrement then leaves -(steps_left - 1))
+  L.steps_left = step_done ? 2 - L.steps_left : -L.steps_left;
+  L.pz = __int_as_float(0x7fffffff);
+}
+
 template <class C, bool PEND>
 __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
                                           const Tables<C::SMEM> &T, const Occ &O,
                                           const NatParams &p, float z, uint32_t u) {
-  if (PEND && L.x < 0.0f) {  // pending hit: the trip stored -px in x (x > 0 before a hit)
+  constexpr bool NEG = PEND && GSDE_STAR_NEG;
+  if constexpr (NEG) {
+    const bool pend = L.steps_left < 0 && !isnan(L.pz);
+    L.steps_left = abs(L.steps_left);
+    if (pend) {  // pending hit: x is its start point
+      L.px = L.x;
+      L.dtr = fmaxf(L.split_factor(G) * L.dtr, 0.0f);
+      L.sq = fast_sqrt(L.dtr);
+    }
+  } else if (PEND && L.x < 0.0f) {  // pending hit: the trip stored -px in x (x > 0 before a hit)
     L.px = -L.x;
     L.dtr = fmaxf(L.split_factor(G) * L.dtr, 0.0f);
     L.sq = fast_sqrt(L.dtr);
@@ -556,6 +579,7 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
   const float xn = C::ZD ? (L.sig * L.sq) * w : fmaf(L.sig * L.sq, w, mu0 * L.dtr);
   if (C::ZD || xn >= 0.0f) {
     L.x = (C::REFLECT && xn > p.reflect) ? fmaxf(2.0f * p.reflect - xn, 0.0f) : xn;
+    if (NEG && !(L.x > 0.0f)) flag_at_vertex(L, true);  // (no residual time left: x == 0)
     return true;
   }
   // failed excursion: dt' = (1 - alpha) dt with alpha = w^2 sig^2 / (mu0^2 dt)
@@ -568,12 +592,14 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
     L.dtr = fmaf(-(w * w), L.kex, L.dtr);
   }
   L.x = 0.0f;
-  if (L.dtr <= 0.0f) return true;
-  if (L.M >= p.cap) {
-    L.trunc = true;
+  const bool ends = L.dtr <= 0.0f || L.M >= p.cap;
+  if (ends) {
+    L.trunc = L.dtr > 0.0f;
+    if (NEG) flag_at_vertex(L, true);
     return true;
   }
   L.sq = fast_sqrt(L.dtr);
+  if (NEG) flag_at_vertex(L, false);
   return false;
 }
 
@@ -682,9 +708,10 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
   // star: live lanes with x <= 0 sit at the vertex (x = -start: a pending hit);
   // general: steps_left > 0 <=> strictly inside the edge (at-vertex lanes carry
   // steps_left < 0), so the common path tests one integer
+  constexpr bool XSIGN = C::STAR && !GSDE_STAR_NEG;  // (the round-1 star encoding)
   const bool live = L.steps_left > 0;
-  const bool run = C::STAR ? live && (L.x > 0.0f) : live;
-  const bool vtx = C::STAR ? live && !run : L.steps_left < 0;  // (before this trip's hit)
+  const bool run = XSIGN ? live && (L.x > 0.0f) : live;
+  const bool vtx = XSIGN ? live && !run : L.steps_left < 0;  // (before this trip's hit)
   if constexpr (C::INJ)  // one injected normal per proposal
     z = run ? L.inj_gauss() : 0.0f;
   float xn = fmaf(L.sig_sqdt, z, C::ZD ? L.x : fmaf(L.drift(G, L.x), p.dt, L.x));
@@ -694,14 +721,20 @@ __device__ __forceinline__ bool trip(Lane<C> &L, const NativeGraph &G,
   if (C::REFLECT && xn > L.len) xn = fmaxf(2.0f * L.len - xn, 0.0f);
   if (hit) {
     L.pz = z;
-    if (C::STAR)  // star: the pending flag and start point live in x's sign
+    if (XSIGN)  // the flag and start point in x's sign
       L.x = -L.x;
-    else  // general: the flag in the step count's sign, x stays the start
+    else  // the flag in the step count's sign, x stays the start
       L.steps_left = -L.steps_left;
   }
   if (ok) {
     L.x = xn;
     L.steps_left -= 1;
+  }
+  // star mirror wall: a proposal reflected onto the vertex itself (x == 0)
+  // starts the next step there (kernels.py:185-188 then :196)
+  if (C::REFLECT && !XSIGN && ok && !(xn > 0.0f) && L.steps_left > 0) {
+    L.steps_left = -L.steps_left;
+    L.pz = __int_as_float(0x7fffffff);
   }
   bool done = ok;
   if (SLOT && vtx) {
@@ -764,7 +797,7 @@ __device__ __forceinline__ void start_particle(Lane<C> &L, const Tables<C::SMEM>
   L.M = 0;
   L.trunc = false;
   L.steps_left = p.n_steps;
-  if (!C::STAR && !(x > 0.0f && x < L.len)) {  // starts at a vertex (see trip)
+  if (C::STAR ? GSDE_STAR_NEG && !(x > 0.0f) : !(x > 0.0f && x < L.len)) {  // at a vertex (trip)
     L.steps_left = -p.n_steps;
     L.pz = __int_as_float(0x7fffffff);
   }
