@@ -354,12 +354,13 @@ def test_occupation_density_beats_snapshot_l2(kind):
         assert eo < 0.05
 
 
-def test_pipelined_run_ensemble_equals_single_launch():
+@pytest.mark.parametrize("steps", [20, 300])  # transfer-bound / kernel-bound chunk schedule
+def test_pipelined_run_ensemble_equals_single_launch(steps):
     """run_ensemble splits large runs by particle id to overlap transfers with
     the next chunk's kernel; the result must equal one launch bit for bit."""
     g, f = workloads.hub64()
     n = (1 << 22) + 12_345
-    cfg = gs.SimulationConfig(dt=1e-3, n_steps=20, n_particles=n, seed=8,
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=steps, n_particles=n, seed=8,
                               initial=gs.PerEdgeUniform(2.0))
     r = gs.run_ensemble(g, f, cfg)
     d = engine.ensemble_device(g, f, cfg, outputs=("edge", "x", "crossings", "events"))
