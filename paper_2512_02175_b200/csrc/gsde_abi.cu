@@ -266,7 +266,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   tabx32[0] = tabmu32[0] = 0.0f;
 
   // --- host-side packing (into the pinned staging buffer) -----------------
-  bool has_tab = false, zero_drift = true;
+  bool has_tab = false, zero_drift = true, const_drift = true;
   for (int64_t e = 0; e < E; ++e) {
     einit[e] = (int32_t)d->edge_init[e];
     eterm[e] = (int32_t)d->edge_term[e];
@@ -279,6 +279,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     sig32[e] = (float)d->sigma[e];
     if (kind[e] == 2) has_tab = true;
     if (kind[e] == 2 || d->dcoef[e] != 0.0) zero_drift = false;
+    if (kind[e] == 2 || (kind[e] == 1 && d->dcoef[e] != 0.0)) const_drift = false;
     if (kind[e] > 2) return set_error(GSDE_EINVAL, "graph_create: bad drift kind on edge %lld",
                                       (long long)e);
   }
@@ -395,6 +396,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   g->is_star = d->is_star != 0;
   g->has_tab = has_tab;
   g->zero_drift = zero_drift;
+  g->const_drift = const_drift;
   g->arena = dev;
   g->arena_bytes = (int64_t)arena_bytes;
   g->work = (unsigned long long *)P(o_work);

@@ -222,7 +222,7 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 
 // Compile-time kernel variant.
 template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false,
-          bool INJ_ = false, bool FULL_ = false, bool PP_ = true>
+          bool INJ_ = false, bool FULL_ = false, bool PP_ = true, bool CD_ = false>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
@@ -251,6 +251,12 @@ struct Cfg {
   // run totals from the block's M histogram + the shared truncation counter
   // (every kernel but FULL -- global M bins -- and INJ -- overrun counts)
   static constexpr bool HT = !FULL_ && !INJ_;
+  // every drift constant in x (general graphs; advection fields such as C4's
+  // drift from_flux): mu(x) = mu_a, the proposal one FFMA shorter and the
+  // lane one register lighter -- bit-identical to the generic kernel, whose
+  // fmaf(mu_b = 0, x, mu_a) is exactly mu_a
+  static constexpr bool CD = CD_;
+  static_assert(!(CD_ && (TAB_ || ZD_)), "constant drift excludes tabulated / zero drift");
   static_assert(PP_ || !(INJ_ || FULL_), "INJ / FULL kernels keep per-particle counters");
   using Cnt = std::conditional_t<FULL_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
@@ -473,6 +479,7 @@ struct Lane {
 
   __device__ __forceinline__ float drift(const NativeGraph &G, float at) const {
     if (C::ZD) return 0.0f;
+    if (C::CD) return mu_a;
     if (C::TAB && isnan(mu_b)) return drift_tab(G, e, at);
     return fmaf(mu_b, at, mu_a);
   }
@@ -1338,36 +1345,31 @@ cudaError_t prepare(K kernel, size_t smem) {
 // ENS: ensemble launches (the lean, no-per-particle-counter kernels exist only there)
 template <bool OCC, bool ENS = false, class F>
 cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
-                     bool inj = false, bool full = false, bool pp = true) {
+                     bool inj = false, bool full = false, bool pp = true, bool cd = false) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
     constexpr bool ST = decltype(st)::value, SM = decltype(sm)::value;
     auto drift = [&](auto rf) -> cudaError_t {
       constexpr bool RF = decltype(rf)::value;
-      if (inj) {  // parity mode: no occupation sampling, 32-bit counts
-        if constexpr (!OCC) {
-          // (INJ kernels carry state-in and the counter; 32-bit counts)
-          if (tab) return f(Cfg<ST, SM, true, RF, false, false, true>{});
-          return zd ? f(Cfg<ST, SM, false, RF, false, true, true>{})
-                    : f(Cfg<ST, SM, false, RF, false, false, true>{});
-        }
+      // drift kind: tabulated / zero / constant (general-graph ensembles) / affine
+      auto mk = [&](auto inj_t, auto full_t, auto pp_t) -> cudaError_t {
+        constexpr bool I = decltype(inj_t)::value, FU = decltype(full_t)::value,
+                       P = decltype(pp_t)::value;
+        if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, I, FU, P>{});
+        if (zd) return f(Cfg<ST, SM, false, RF, OCC, true, I, FU, P>{});
+        if constexpr (ENS && !ST)
+          if (cd) return f(Cfg<ST, SM, false, RF, OCC, false, I, FU, P, true>{});
+        return f(Cfg<ST, SM, false, RF, OCC, false, I, FU, P>{});
+      };
+      if (inj) {  // parity mode: no occupation sampling; state-in, counter, 32-bit counts
+        if constexpr (!OCC) return mk(T{}, N{}, T{});
         return cudaErrorInvalidValue;
       }
-      if (full) {
-        if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, true>{});
-        return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, true>{})
-                  : f(Cfg<ST, SM, false, RF, OCC, false, false, true>{});
-      }
-      if constexpr (ENS) {
-        if (!pp) {  // lean: fused estimators only
-          if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, false, false, false>{});
-          return zd ? f(Cfg<ST, SM, false, RF, OCC, true, false, false, false>{})
-                    : f(Cfg<ST, SM, false, RF, OCC, false, false, false, false>{});
-        }
-      }
-      if (tab) return f(Cfg<ST, SM, true, RF, OCC>{});
-      return zd ? f(Cfg<ST, SM, false, RF, OCC, true>{}) : f(Cfg<ST, SM, false, RF, OCC>{});
+      if (full) return mk(N{}, T{}, T{});
+      if constexpr (ENS)
+        if (!pp) return mk(N{}, N{}, N{});  // lean: fused estimators only
+      return mk(N{}, N{}, T{});
     };
     if constexpr (ST)
       if (reflect) return drift(T{});
@@ -1492,9 +1494,9 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   // per-particle counters only when some per-particle array is requested
   const bool pp = o.edge || o.x || o.crossings || o.events || o.truncs;
   return occ ? dispatch<true, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
-                              inj, full, pp)
+                                    inj, full, pp, g->const_drift)
              : dispatch<false, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                               run, inj, full, pp);
+                                     run, inj, full, pp, g->const_drift);
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
