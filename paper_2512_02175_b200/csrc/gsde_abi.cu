@@ -266,7 +266,17 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   tabx32[0] = tabmu32[0] = 0.0f;
 
   // --- host-side packing (into the pinned staging buffer) -----------------
+  // validation first (the packing loops below run in parallel: OpenMP over
+  // edges / slots / vertices for large networks -- a 1e5-edge upload)
+  for (int64_t e = 0; e < E; ++e)
+    if (d->dkind[e] < 0 || d->dkind[e] > 2)
+      return set_error(GSDE_EINVAL, "graph_create: bad drift kind on edge %lld", (long long)e);
+  for (int64_t v = 0; v < V; ++v)
+    if (d->v_off[v + 1] - d->v_off[v] < 1)
+      return set_error(GSDE_EINVAL, "graph_create: vertex %lld has no slots", (long long)v);
+  const bool par = E + S > 32768;
   bool has_tab = false, zero_drift = true, const_drift = true;
+#pragma omp parallel for if (par) reduction(|| : has_tab) reduction(&& : zero_drift, const_drift)
   for (int64_t e = 0; e < E; ++e) {
     einit[e] = (int32_t)d->edge_init[e];
     eterm[e] = (int32_t)d->edge_term[e];
@@ -277,11 +287,9 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     coef32[e] = (float)d->dcoef[e];
     sig64[e] = d->sigma[e];
     sig32[e] = (float)d->sigma[e];
-    if (kind[e] == 2) has_tab = true;
-    if (kind[e] == 2 || d->dcoef[e] != 0.0) zero_drift = false;
-    if (kind[e] == 2 || (kind[e] == 1 && d->dcoef[e] != 0.0)) const_drift = false;
-    if (kind[e] > 2) return set_error(GSDE_EINVAL, "graph_create: bad drift kind on edge %lld",
-                                      (long long)e);
+    has_tab = has_tab || kind[e] == 2;
+    zero_drift = zero_drift && !(kind[e] == 2 || d->dcoef[e] != 0.0);
+    const_drift = const_drift && !(kind[e] == 2 || (kind[e] == 1 && d->dcoef[e] != 0.0));
   }
   for (int64_t e = 0; e <= E; ++e) taboff[e] = (int32_t)d->tab_off[e];
   for (int64_t t = 0; t < T; ++t) {
@@ -292,6 +300,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   }
   for (int64_t v = 0; v <= V; ++v) voff[v] = (int32_t)d->v_off[v];
   const double two53 = 9007199254740992.0;
+#pragma omp parallel for if (par)
   for (int64_t j = 0; j < S; ++j) {
     vedges[j] = (int32_t)d->v_edges[j];
     vorient[j] = (uint8_t)d->v_orient[j];
@@ -301,6 +310,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     thresh[j] = (uint64_t)c;
   }
   // native records
+#pragma omp parallel for if (par)
   for (int64_t e = 0; e < E; ++e) {
     float4 r;
     // FP32 length rounded toward zero, so every native position (<= the FP32
@@ -334,30 +344,33 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
     nedgev[e] = make_int4(voff[a], voff[a + 1] - voff[a], b >= 0 ? voff[b] : 0,
                           b >= 0 ? voff[b + 1] - voff[b] : 0);
   }
-  std::vector<double> prob;
-  std::vector<int> alias;
-  for (int64_t v = 0; v < V; ++v) {
-    const int lo = voff[v], deg = voff[v + 1] - voff[v];
-    if (deg < 1) return set_error(GSDE_EINVAL, "graph_create: vertex %lld has no slots",
-                                  (long long)v);
-    build_alias(d->v_weights + lo, deg, prob, alias);
-    for (int j = 0; j < deg; ++j) {
-      const int sp = lo + j, sa = lo + alias[j];
-      const uint32_t prim = (uint32_t)vedges[sp] | ((uint32_t)vorient[sp] << 31);
-      const uint32_t alt = (uint32_t)vedges[sa] | ((uint32_t)vorient[sa] << 31);
-      double t = std::nearbyint(prob[j] * 4294967296.0);
-      uint32_t th = t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)(t > 0.0 ? t : 0.0);
-      int4 c;
-      c.x = (int)th;
-      c.y = (int)prim;
-      c.z = (int)(prob[j] >= 1.0 ? prim : alt);
-      c.w = 0;
-      ncol[sp] = c;
+#pragma omp parallel if (par)
+  {
+    std::vector<double> prob;
+    std::vector<int> alias;
+#pragma omp for schedule(static, 1024)
+    for (int64_t v = 0; v < V; ++v) {
+      const int lo = voff[v], deg = voff[v + 1] - voff[v];
+      build_alias(d->v_weights + lo, deg, prob, alias);
+      for (int j = 0; j < deg; ++j) {
+        const int sp = lo + j, sa = lo + alias[j];
+        const uint32_t prim = (uint32_t)vedges[sp] | ((uint32_t)vorient[sp] << 31);
+        const uint32_t alt = (uint32_t)vedges[sa] | ((uint32_t)vorient[sa] << 31);
+        double t = std::nearbyint(prob[j] * 4294967296.0);
+        uint32_t th = t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)(t > 0.0 ? t : 0.0);
+        int4 c;
+        c.x = (int)th;
+        c.y = (int)prim;
+        c.z = (int)(prob[j] >= 1.0 ? prim : alt);
+        c.w = 0;
+        ncol[sp] = c;
+      }
     }
   }
   lap("records + alias tables");
   // fat alias columns for general graphs (one L2 round trip per vertex event)
   if (!d->is_star) {
+#pragma omp parallel for if (par)
     for (int64_t j = 0; j < S; ++j) {
       const int4 c = ncol[j];
       const int pe = c.y & 0x7fffffff, ae = c.z & 0x7fffffff;
