@@ -797,6 +797,8 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # communicator setup (nranks, NVLS / NVLink transport) in the log
         os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # (NCCL logs to stdout by default: keep stdout for the one JSON line)
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if shared:
             tdist.init_process_group("gloo")
         else:
