@@ -1309,6 +1309,13 @@ bool force_global_bins() {
   static const bool f = std::getenv("GSDE_FORCE_GLOBAL_BINS") != nullptr;
   return f;
 }
+// Testing knob: GSDE_GENERIC_DRIFT=1 runs constant-drift graphs through the
+// generic affine-drift kernel (the constant-drift variant must match it bit
+// for bit: tests/test_gpu_robustness.py).
+bool generic_drift() {
+  static const bool f = std::getenv("GSDE_GENERIC_DRIFT") != nullptr;
+  return f;
+}
 
 NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
   NatParams p{};
@@ -1494,9 +1501,9 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   // per-particle counters only when some per-particle array is requested
   const bool pp = o.edge || o.x || o.crossings || o.events || o.truncs;
   return occ ? dispatch<true, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
-                                    inj, full, pp, g->const_drift)
+                                    inj, full, pp, g->const_drift && !generic_drift())
              : dispatch<false, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                                     run, inj, full, pp, g->const_drift);
+                                     run, inj, full, pp, g->const_drift && !generic_drift());
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,

@@ -162,3 +162,52 @@ def test_global_bins_path_equals_shared_counters(tmp_path):
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
     assert a["hub64_lean_m_hist"][4] > 0  # steps at the cap are counted
+
+
+_CD_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import engine, workloads
+out = {{}}
+g, f = workloads.vascular(20_000, seed=5)
+grid = gs.EdgeGrid.uniform(g, 4)
+for cap in (100, 3):
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=200, n_particles=300_001, seed=3,
+                              initial=gs.PerEdgeUniform(float(g.edge_length.max())),
+                              max_splits_per_step=cap)
+    for outs in (("edge_counts",), ("all", "edge_counts")):
+        r = engine.ensemble_device(g, f, cfg, outputs=outs, grid=grid, occupation=(5, 2))
+        for k, v in r.items():
+            if not k.startswith("_") and v is not None:
+                out["c%d_%d_%s" % (cap, len(outs), k)] = v.cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_constant_drift_variant_equals_generic_kernel(tmp_path):
+    """Graphs whose drifts are all constant in x (C4's drift from_flux) run the
+    constant-drift kernel variant; it must equal the generic affine-drift kernel
+    (GSDE_GENERIC_DRIFT=1) bit for bit, lean and per-particle, with occupation
+    sampling and a truncating cap."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for generic in (False, True):
+        path = str(tmp_path / f"cd_{int(generic)}.npz")
+        env = dict(os.environ)
+        env.pop("GSDE_GENERIC_DRIFT", None)
+        if generic:
+            env["GSDE_GENERIC_DRIFT"] = "1"
+        subprocess.run([sys.executable, "-c", _CD_SCRIPT.format(root=root, path=path)],
+                       check=True, env=env, timeout=600)
+        res[generic] = np.load(path)
+    a, b = res[False], res[True]
+    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 20
+    for k in a.files:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
