@@ -1399,8 +1399,9 @@ bool ensemble_needs_full(const gsde_run &a, const gsde_out &o) {
 
 }  // namespace
 
-cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const gsde_out &o,
-                                   cudaStream_t s) {
+namespace {
+cudaError_t launch_native_ensemble_one(const gsde_graph *g, const gsde_run &a, const gsde_out &o,
+                                       cudaStream_t s) {
   NatParams p = make_params(a.seed, a.n_particles, a.pid_offset, a.dt, a.cap);
   p.n_steps = (int32_t)a.n_steps;
   p.reflect = (float)a.reflect_len;
@@ -1504,6 +1505,51 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
                                     inj, full, pp, g->const_drift && !generic_drift())
              : dispatch<false, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
                                      run, inj, full, pp, g->const_drift && !generic_drift());
+}
+
+}  // namespace
+
+// A call whose particles would let one block count 2^32 events in a shared
+// 32-bit counter (launch_native_ensemble_one's bound: per-warp budget x steps)
+// runs as consecutive launches over contiguous particle-id chunks small enough
+// to keep the shared counters -- results are bit-identical (streams are keyed
+// by global id; estimators accumulate) -- instead of taking the FULL kernel's
+// global-memory counters, whose same-address atomics would serialise a large
+// run.  Only when a single chunk of the minimum size would still overflow
+// (n_steps beyond ~1.6e6) does the run fall back to global counters.
+// GSDE_CHUNK_PARTICLES=<n> forces chunks of n particles (testing).
+cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const gsde_out &o,
+                                   cudaStream_t s) {
+  const int64_t n = a.n_particles;
+  const double steps = (double)std::max<int64_t>(a.n_steps, 1);
+  const double sm8 = 8.0 * dev_info(g->device).sm_count;
+  // launch_native_ensemble_one's share(nc) = 8 (max(256, 4 ceil(nc / sm8)) + 64)
+  // stays below 2^32 / steps for ceil(nc / sm8) <= lim
+  const double lim = std::floor((4294967295.0 / (8.0 * steps) - 64.0) / 4.0) - 1.0;
+  int64_t chunk = lim >= 256.0 ? (int64_t)std::min(lim * sm8, 9.0e18) : 0;
+  static const char *forced = std::getenv("GSDE_CHUNK_PARTICLES");
+  if (forced && std::atoll(forced) > 0) chunk = std::atoll(forced);
+  if (chunk <= 0 || n <= chunk) return launch_native_ensemble_one(g, a, o, s);
+  for (int64_t off = 0; off < n; off += chunk) {
+    gsde_run ac = a;
+    ac.n_particles = std::min(chunk, n - off);
+    ac.pid_offset = a.pid_offset + off;
+    if (ac.inj_raw) ac.inj_raw += off * a.inj_stride;
+    if (ac.inj_normal) ac.inj_normal += off * a.inj_stride;
+    if (ac.state_edge) ac.state_edge += off;
+    if (ac.state_x) ac.state_x += off;
+    if (ac.state_counter) ac.state_counter += off;
+    gsde_out oc = o;
+    if (oc.edge) oc.edge += off;
+    if (oc.x) oc.x += off;
+    if (oc.crossings) oc.crossings += off;
+    if (oc.events) oc.events += off;
+    if (oc.truncs) oc.truncs += off;
+    if (oc.counter) oc.counter += off;
+    const cudaError_t err = launch_native_ensemble_one(g, ac, oc, s);
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,

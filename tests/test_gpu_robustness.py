@@ -211,3 +211,68 @@ def test_constant_drift_variant_equals_generic_kernel(tmp_path):
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
 
+
+_CHUNK_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import torch
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import engine, workloads
+out = {{}}
+for name, (g, f), init in (("hub64", workloads.hub64(), gs.PerEdgeUniform(2.0)),
+                           ("star3", workloads.star3(), gs.AtVertex(0))):
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=150, n_particles=100_003, seed=3, initial=init,
+                              max_splits_per_step=4)
+    grid = gs.EdgeGrid.uniform(g, 4, lengths=[3.0] * g.n_edges if g.is_star else None)
+    for outs in (("edge_counts",), ("all", "edge_counts", "counter")):
+        r = engine.ensemble_device(g, f, cfg, outputs=outs, grid=grid, occupation=(3, 1))
+        for k, v in r.items():
+            if not k.startswith("_") and v is not None:
+                out[name + "_%d_" % len(outs) + k] = v.cpu().numpy()
+    # resume from state-in (per-particle edge / x / next Philox block): pointer offsets
+    st = (r["edge"].to(torch.int32), r["x"].to(torch.float32), r["counter"])
+    r2 = engine.ensemble_device(g, f, cfg, outputs=("all", "counter"), state=st)
+    for k in ("edge", "x", "crossings", "counter", "m_hist", "totals"):
+        out[name + "_resume_" + k] = r2[k].cpu().numpy()
+# injected reference draws through the production kernel (row pointer offsets)
+g, f = workloads.hub64()
+rs = np.random.default_rng(3)
+n, K = 20_001, 120
+raw = torch.as_tensor(rs.integers(0, 2**63, size=(n, K), dtype=np.int64)).cuda()
+nrm = torch.as_tensor(rs.standard_normal((n, K))).cuda()
+cfg = gs.SimulationConfig(dt=1e-3, n_steps=40, n_particles=n, seed=3,
+                          initial=gs.PerEdgeUniform(2.0))
+r = engine.ensemble_device(g, f, cfg, inject=(raw, nrm), precision="native",
+                           outputs=("all", "counter"))
+for k in ("edge", "x", "crossings", "counter", "m_hist", "totals"):
+    out["inj_" + k] = r[k].cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_chunked_launches_equal_one_launch(tmp_path):
+    """Calls large enough to overflow a block's 32-bit shared counters run as
+    consecutive launches over particle-id chunks; GSDE_CHUNK_PARTICLES forces
+    small chunks.  Estimators, per-particle arrays, the native resume path
+    (state-in + Philox counters) and injected-draw rows must equal one launch."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for chunk in (None, "7777"):
+        path = str(tmp_path / f"chunk_{chunk}.npz")
+        env = dict(os.environ)
+        env.pop("GSDE_CHUNK_PARTICLES", None)
+        if chunk:
+            env["GSDE_CHUNK_PARTICLES"] = chunk
+        subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT.format(root=root, path=path)],
+                       check=True, env=env, timeout=600)
+        res[chunk] = np.load(path)
+    a, b = res[None], res["7777"]
+    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 30
+    for k in a.files:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
