@@ -1525,8 +1525,11 @@ cudaError_t launch_native_ensemble(const gsde_graph *g, const gsde_run &a, const
   const double sm8 = 8.0 * dev_info(g->device).sm_count;
   // launch_native_ensemble_one's share(nc) = 8 (max(256, 4 ceil(nc / sm8)) + 64)
   // stays below 2^32 / steps for ceil(nc / sm8) <= lim
+  // (share never drops below 8 (256 + 64): chunks help while that x steps fits)
   const double lim = std::floor((4294967295.0 / (8.0 * steps) - 64.0) / 4.0) - 1.0;
-  int64_t chunk = lim >= 256.0 ? (int64_t)std::min(lim * sm8, 9.0e18) : 0;
+  int64_t chunk = 8.0 * (256.0 + 64.0) * steps < 4294967295.0
+                      ? (int64_t)std::min(std::max(lim, 1.0) * sm8, 9.0e18)
+                      : 0;
   static const char *forced = std::getenv("GSDE_CHUNK_PARTICLES");
   if (forced && std::atoll(forced) > 0) chunk = std::atoll(forced);
   if (chunk <= 0 || n <= chunk) return launch_native_ensemble_one(g, a, o, s);
