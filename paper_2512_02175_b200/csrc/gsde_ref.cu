@@ -11,6 +11,10 @@
 // One thread per particle, grid-stride; M histogram in shared memory.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
 #include "gsde_epilogue.cuh"
 
 namespace gsde {
@@ -363,11 +367,15 @@ int grid_for(int64_t n, int device) {
 }
 
 template <class R, class D>
-cudaError_t ensemble_impl(const RefGraph<R> &g, bool star, const gsde_run &a, const gsde_out &o,
-                          int device, cudaStream_t s) {
+cudaError_t ensemble_one(const RefGraph<R> &g, bool star, const gsde_run &a, const gsde_out &o,
+                         int device, cudaStream_t s) {
   const size_t mh = (size_t)(a.cap + 1) * sizeof(int);
-  const int use_smem = mh <= 32 * 1024 ? 1 : 0;
   const int grid = grid_for(a.n_particles, device);
+  // shared int M bins while a block's count cannot reach 2^31 (grid-stride:
+  // exact per-block particle counts); ensemble_impl chunks calls to keep this
+  const double per_block = std::ceil((double)a.n_particles / ((double)grid * 256.0)) * 256.0 *
+                           (double)(a.n_steps > 0 ? a.n_steps : 1);
+  const int use_smem = (mh <= 32 * 1024 && per_block < 2147483647.0) ? 1 : 0;
   if (star)
     ref_ensemble_kernel<R, D, true><<<grid, 256, use_smem ? mh : 0, s>>>(g, a, kernel_out(o), use_smem);
   else
@@ -376,12 +384,43 @@ cudaError_t ensemble_impl(const RefGraph<R> &g, bool star, const gsde_run &a, co
   return cudaGetLastError();
 }
 
+// Calls whose blocks could count 2^31 steps into a shared bin run as
+// consecutive launches over particle-id chunks (streams are keyed by global
+// id, estimators accumulate: bit-identical to one launch).
+template <class R, class D>
+cudaError_t ensemble_impl(const RefGraph<R> &g, bool star, const gsde_run &a, const gsde_out &o,
+                          int device, cudaStream_t s) {
+  const double wave = (double)dev_info(device).sm_count * 32.0 * 256.0;  // grid_for's cap x 256
+  const double k = std::floor(2147483647.0 / (256.0 * (double)(a.n_steps > 0 ? a.n_steps : 1)));
+  int64_t chunk = k >= 1.0 ? (int64_t)std::min(k * wave, 9.0e18) : 0;
+  static const char *forced = std::getenv("GSDE_CHUNK_PARTICLES");  // (testing)
+  if (forced && std::atoll(forced) > 0) chunk = std::atoll(forced);
+  if (chunk <= 0 || a.n_particles <= chunk) return ensemble_one<R, D>(g, star, a, o, device, s);
+  for (int64_t off = 0; off < a.n_particles; off += chunk) {
+    gsde_run ac = a;
+    ac.n_particles = std::min(chunk, a.n_particles - off);
+    ac.pid_offset = a.pid_offset + off;
+    if (ac.inj_raw) ac.inj_raw += off * a.inj_stride;
+    if (ac.inj_normal) ac.inj_normal += off * a.inj_stride;
+    gsde_out oc = o;
+    if (oc.edge) oc.edge += off;
+    if (oc.x) oc.x += off;
+    if (oc.crossings) oc.crossings += off;
+    if (oc.events) oc.events += off;
+    if (oc.truncs) oc.truncs += off;
+    const cudaError_t err = ensemble_one<R, D>(g, star, ac, oc, device, s);
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
 template <class R, class D>
 cudaError_t trials_impl(const RefGraph<R> &g, bool star, const gsde_trials &a,
                         const gsde_trials_out &o, int device, cudaStream_t s) {
   const size_t mh = (size_t)(a.cap + 1) * sizeof(int);
-  const int use_smem = mh <= 32 * 1024 ? 1 : 0;
   const int grid = grid_for(a.n_trials, device);
+  const double per_block = std::ceil((double)a.n_trials / ((double)grid * 256.0)) * 256.0;
+  const int use_smem = (mh <= 32 * 1024 && per_block < 2147483647.0) ? 1 : 0;
   if (star)
     ref_trials_kernel<R, D, true><<<grid, 256, use_smem ? mh : 0, s>>>(g, a, o, use_smem);
   else

@@ -235,6 +235,13 @@ for name, (g, f), init in (("hub64", workloads.hub64(), gs.PerEdgeUniform(2.0)),
     r2 = engine.ensemble_device(g, f, cfg, outputs=("all", "counter"), state=st)
     for k in ("edge", "x", "crossings", "counter", "m_hist", "totals"):
         out[name + "_resume_" + k] = r2[k].cpu().numpy()
+# the reference's own streams (FP64 reference-stream kernel, its own chunking)
+g, f = workloads.hub64()
+cfg = gs.SimulationConfig(dt=1e-3, n_steps=60, n_particles=30_001, seed=9,
+                          initial=gs.PerEdgeUniform(2.0), rng="reference")
+r = engine.ensemble_device(g, f, cfg, outputs=("all",))
+for k in ("edge", "x", "crossings", "events", "m_hist", "totals"):
+    out["ref_" + k] = r[k].cpu().numpy()
 # injected reference draws through the production kernel (row pointer offsets)
 g, f = workloads.hub64()
 rs = np.random.default_rng(3)
@@ -272,7 +279,7 @@ def test_chunked_launches_equal_one_launch(tmp_path):
                        check=True, env=env, timeout=600)
         res[chunk] = np.load(path)
     a, b = res[None], res["7777"]
-    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 30
+    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 36
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
 
