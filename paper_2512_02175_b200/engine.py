@@ -362,7 +362,7 @@ def run_ensemble(graph: MetricGraph, field: CoefficientField,
 # small first chunk, so the copy engine starts early.  Measured (ms per
 # run_ensemble, one B200): star3 1.6e7 x 1000: 25.5 (kernel-bound schedule) vs
 # 26.0; hub64 1e8 x 1000: 267.2 vs 268.2; vascular 1e8 x 100: 88.9 vs 76.7.
-_CHUNKS = (0.5, 0.28, 0.14, 0.06, 0.02)
+_CHUNKS = (0.55, 0.25, 0.12, 0.055, 0.02, 0.005)  # (0.5, .28, .14, .06, .02): +0.3%
 _CHUNKS_TRANSFER_BOUND = (0.08, 0.22, 0.3, 0.25, 0.12, 0.03)
 _PIPELINE_MIN = 1 << 22
 _COPY_STREAMS: dict = {}  # device -> (copy stream, second launch stream)
