@@ -259,6 +259,25 @@ class FvmWork(Workload):
     def crossings(self, res):
         return 0
 
+    def e2e_call(self):
+        """``fvm.fvm_run`` with a host initial state: the CFL check, the static
+        packing (not reused across calls: inputs travel every call), the upload,
+        every step on the GPU and the host copy of the final density."""
+        from paper_2512_02175_b200 import fvm
+
+        fvm._PACK_MEMO.clear()
+        r = fvm.fvm_run(self.g, self.f, self.grid, self.dt, self.n_steps,
+                        fvm.FvmState.uniform(self.grid))
+        return r.state.rho.nbytes
+
+    def e2e_h2d(self):
+        return int(sum(getattr(self.fd.packed, k).nbytes for k in _FVM_DESC)) + \
+            8 * self.grid.n_cells
+
+    def e2e_path(self):
+        return ("paper_2512_02175_b200.fvm.fvm_run (C-ABI gsde_fvm_run): CFL check, static "
+                "packing, upload, all steps on the GPU, D2H of the final density")
+
     def cpu_baseline(self, steps=20):
         """The reference's own FVM stepper (``graphsde.fvm._fvm_step_loop``, numba,
         single-threaded by design, fvm.py:253-340) on the same C4 grid, fed the
@@ -288,6 +307,11 @@ class FvmWork(Workload):
         return {"value": self.grid.n_cells * 10 / (time.perf_counter() - t0), "unit": self.unit,
                 "cores": 1, "kind": "port", "reference_unavailable": why,
                 "sample": "10 steps, oracle/gsde_oracle.c orc_fvm_steps (single thread)"}
+
+
+_FVM_DESC = ("cell_mu_l", "cell_mu_r", "cell_D", "cell_dx", "cell_flags", "v_off", "v_cells",
+             "v_b", "v_dx", "v_speed_in", "v_D", "slot_vertex", "pslot", "vser", "tstart",
+             "rstart", "rpos")
 
 
 def make_workload(name, rank, world):
@@ -724,9 +748,10 @@ def measure_e2e(wl, steps, warmup, dist, torch, dev, world):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t[0])
         times.append(el)
-    dg = _native.device_graph(wl.g, wl.f, dev)
+    h2d = wl.e2e_h2d() if hasattr(wl, "e2e_h2d") else \
+        int(_native.device_graph(wl.g, wl.f, dev).device_bytes)
     return {"value": wl.units_per_step * world * len(times) / sum(times), "unit": wl.unit,
-            "h2d_bytes_per_step": int(dg.device_bytes) * world,
+            "h2d_bytes_per_step": int(h2d) * world,
             "d2h_bytes_per_step": int(nbytes) * world,
             "ms_per_call": [round(t * 1e3, 2) for t in times], "path": wl.e2e_path()}
 
@@ -744,6 +769,7 @@ def extra_line(name, torch, dev, flush_buf, peaks, peak_ops, with_cpu):
             "bytes_per_cell_step": bpc, "achieved_gbs": rate2 * bpc / 1e9,
             "frac_of_hbm_peak": rate2 * bpc / 1e9 / float(peaks.get("hbm_gbs", 7700)),
             "note": "working set (~40 MB) is L2-resident across steps",
+            "e2e": measure_e2e(w2, 3, 1, None, torch, dev, 1),
             "cpu_baseline": w2.cpu_baseline() if with_cpu else None}
     c2 = w2.crossings(r2) / w2.units_per_step
     out = {"value": rate2, "unit": w2.unit, "config": w2.config(), "step_ms": list(STEP_MS),
