@@ -348,7 +348,7 @@ def _vertex_template(n: int, active):
     return tstart, rows, pos
 
 
-def _term_layout(v_off, v_b, v_speed_in, pslot, slot_vertex):
+def _term_layout(v_off, v_b, v_speed_in, pslot, slot_vertex, bitkey=True):
     """Static layout of the two-phase vertex exchange on the GPU.
 
     Every contribution the reference's exchange loop (``fvm.py:305-328``) adds to
@@ -383,7 +383,7 @@ def _term_layout(v_off, v_b, v_speed_in, pslot, slot_vertex):
     slot_v = np.repeat(np.arange(verts.shape[0], dtype=np.int64), deg)
     local = np.arange(slot_v.shape[0], dtype=np.int64) - np.repeat(base_slot := np.r_[0, np.cumsum(deg)[:-1]], deg)
     gslot = lo[slot_v] + local  # graph slot of every (vertex, local index)
-    if int(deg.max()) <= 60:
+    if bitkey and int(deg.max()) <= 60:
         bits = np.zeros(verts.shape[0], dtype=np.int64)
         np.add.at(bits, slot_v, act[gslot].astype(np.int64) << local)
         code = (bits << 6) | deg
