@@ -241,6 +241,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
                o_thresh = Lo.add(S * 8), o_kind = Lo.add(E), o_taboff = Lo.add((E + 1) * 4),
                o_nedge = Lo.add(E * sizeof(float4)), o_nedgev = Lo.add(E * sizeof(int4)),
                o_ncol = Lo.add(S * sizeof(int4)), o_nfat = Lo.add(nfat * sizeof(int4)),
+               o_nufat = Lo.add((d->is_star ? 0 : (size_t)S * 3) * sizeof(int4)),
                o_work = Lo.add(gsde_graph::kWorkSlots * sizeof(unsigned long long));
   Staging &st = staging();
   std::lock_guard<std::mutex> staging_lock(st.mu);
@@ -260,7 +261,7 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   uint64_t *thresh = at(o_thresh, (uint64_t *)0);
   float4 *nedge = at(o_nedge, (float4 *)0);
   int4 *nedgev = at(o_nedgev, (int4 *)0), *ncol = at(o_ncol, (int4 *)0),
-       *nfat4 = at(o_nfat, (int4 *)0);
+       *nfat4 = at(o_nfat, (int4 *)0), *nufat4 = at(o_nufat, (int4 *)0);
   memset(at(o_work, (unsigned char *)0), 0, gsde_graph::kWorkSlots * sizeof(unsigned long long));
   tabx64[0] = tabmu64[0] = 0.0;
   tabx32[0] = tabmu32[0] = 0.0f;
@@ -382,8 +383,14 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
       nfat4[5 * j + 2] = nedgev[pe];
       nfat4[5 * j + 3] = ae4;
       nfat4[5 * j + 4] = nedgev[ae];
+      nufat4[3 * j + 0] = make_int4(c.y, 0, 0, 0);
+      nufat4[3 * j + 1] = pe4;
+      nufat4[3 * j + 2] = nedgev[pe];
     }
   }
+  // every column's alias is its own slot (prob >= 1: equal jump weights)?
+  bool uniform_exits = true;
+  for (int64_t j = 0; j < S && uniform_exits; ++j) uniform_exits = ncol[j].y == ncol[j].z;
   lap("fat columns");
   size_t arena_bytes = Lo.size;
   void *dev = arena_pool().take(device, Lo.size, &arena_bytes);
@@ -438,6 +445,8 @@ int gsde_graph_create(const gsde_graph_desc *d, int device, gsde_graph **out) {
   g->nat.edgev = (const int4 *)P(o_nedgev);
   g->nat.col = (const int4 *)P(o_ncol);
   g->nat.fat = d->is_star ? nullptr : (const int4 *)P(o_nfat);
+  g->nat.ufat = d->is_star ? nullptr : (const int4 *)P(o_nufat);
+  g->uniform_exits = uniform_exits;
   g->nat.tab_off = (const int32_t *)P(o_taboff);
   g->nat.tab_x = (const float *)P(o_tabx32);
   g->nat.tab_mu = (const float *)P(o_tabmu32);

@@ -206,6 +206,9 @@ struct NativeGraph {
   const int4 *edgev;
   const int4 *col;
   const int4 *fat;  // [S][5]: {thresh, prim, alias, 0}, prim {edge, edgev}, alias {edge, edgev}
+  // [S][3]: {prim, 0, 0, 0}, prim {edge, edgev} -- graphs whose every exit
+  // column keeps its own slot (uniform jump weights): the pick is the column
+  const int4 *ufat;
   const int32_t *tab_off;
   const float *tab_x, *tab_mu;
   int32_t has_tab;

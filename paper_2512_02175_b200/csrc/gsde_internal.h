@@ -15,6 +15,7 @@ struct gsde_graph_s {
   bool has_tab = false;
   bool zero_drift = false;  // every edge driftless (kind 0/1 with coefficient 0)
   bool const_drift = false; // every edge's drift constant in x (kind 0, or kind 1 with 0)
+  bool uniform_exits = false; // every alias column keeps its own slot (equal jump weights)
   void *arena = nullptr;
   int64_t arena_bytes = 0;
   gsde::RefGraph<double> ref64{};

@@ -183,6 +183,7 @@ struct Tables {
   const int4 *edgev;
   const int4 *col;
   const int4 *fat;  // L2 path: fat alias columns
+  const int4 *ufat; // L2 path, uniform exits: {slot, edge record, endpoint record}
   __device__ __forceinline__ float4 E(int e) const { return SMEM ? edge[e] : __ldg(edge + e); }
   __device__ __forceinline__ int4 V(int e) const { return SMEM ? edgev[e] : __ldg(edgev + e); }
   __device__ __forceinline__ int4 C(int j) const { return SMEM ? col[j] : __ldg(col + j); }
@@ -222,7 +223,8 @@ __device__ float drift_tab(const NativeGraph &G, int e, float x) {
 
 // Compile-time kernel variant.
 template <bool STAR_, bool SMEM_, bool TAB_, bool REFLECT_, bool OCC_, bool ZD_ = false,
-          bool INJ_ = false, bool FULL_ = false, bool PP_ = true, bool CD_ = false>
+          bool INJ_ = false, bool FULL_ = false, bool PP_ = true, bool CD_ = false,
+          bool UNI_ = false>
 struct Cfg {
   static constexpr bool STAR = STAR_;        // star graph (one vertex, semi-infinite edges)
   static constexpr bool SMEM = SMEM_;        // graph tables staged in shared memory
@@ -257,6 +259,12 @@ struct Cfg {
   // fmaf(mu_b = 0, x, mu_a) is exactly mu_a
   static constexpr bool CD = CD_;
   static_assert(!(CD_ && (TAB_ || ZD_)), "constant drift excludes tabulated / zero drift");
+  // every exit column keeps its own slot (equal jump weights at every vertex,
+  // as on C2 and C4): the exit pick is the column -- no threshold compare, no
+  // candidate selects, and on L2-resident graphs a 48 B record (the slot and
+  // its edge's records) instead of 80 B; the same slot as the alias pick
+  static constexpr bool UNI = UNI_;
+  static_assert(!(UNI_ && (STAR_ || INJ_)), "uniform exits: general-graph native kernels");
   static_assert(PP_ || !(INJ_ || FULL_), "INJ / FULL kernels keep per-particle counters");
   using Cnt = std::conditional_t<FULL_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
@@ -335,6 +343,7 @@ __device__ __forceinline__ void shared_setup(const NativeGraph &G, int nb, int64
   T.edgev = G.edgev;
   T.col = G.col;
   T.fat = G.fat;
+  T.ufat = G.ufat;
   if (SMEM) {
     float4 *se = reinterpret_cast<float4 *>(smem + off);
     off += (size_t)G.n_edges * sizeof(float4);
@@ -657,9 +666,17 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
     s = ref_pick(L, off, deg, L.inj_raw());
     L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
     z = L.inj_gauss();
+  } else if constexpr (C::SMEM && C::UNI) {
+    s = T.C(off + (int)__umulhi(u, (uint32_t)deg)).y;
+    L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
   } else if constexpr (C::SMEM) {
     s = alias_pick(T, off, deg, u);
     L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
+  } else if constexpr (C::UNI) {  // one round trip: the slot + its edge's records
+    const int4 *f = T.ufat + 3 * (off + (int)__umulhi(u, (uint32_t)deg));
+    const int4 c = __ldg(f), er = __ldg(f + 1), ev = __ldg(f + 2);
+    s = c.x;
+    L.load_edge_rec(O, s & 0x7fffffff, *reinterpret_cast<const float4 *>(&er), ev, p.sqdt);
   } else {  // one round trip: column + both candidates' records in flight together
     uint32_t hi, lo;
     mul_hilo(u, (uint32_t)deg, hi, lo);
@@ -1316,6 +1333,12 @@ bool generic_drift() {
   static const bool f = std::getenv("GSDE_GENERIC_DRIFT") != nullptr;
   return f;
 }
+// Testing knob: GSDE_GENERIC_EXITS=1 picks exits through the alias columns even
+// where every column keeps its own slot (the uniform-exit variant must match).
+bool generic_exits() {
+  static const bool f = std::getenv("GSDE_GENERIC_EXITS") != nullptr;
+  return f;
+}
 
 NatParams make_params(uint64_t seed, int64_t n, int64_t off, double dt, int32_t cap) {
   NatParams p{};
@@ -1352,7 +1375,8 @@ cudaError_t prepare(K kernel, size_t smem) {
 // ENS: ensemble launches (the lean, no-per-particle-counter kernels exist only there)
 template <bool OCC, bool ENS = false, class F>
 cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&f,
-                     bool inj = false, bool full = false, bool pp = true, bool cd = false) {
+                     bool inj = false, bool full = false, bool pp = true, bool cd = false,
+                     bool uni = false) {
   using T = std::true_type;
   using N = std::false_type;
   auto with = [&](auto st, auto sm) -> cudaError_t {
@@ -1369,14 +1393,28 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
           if (cd) return f(Cfg<ST, SM, false, RF, OCC, false, I, FU, P, true>{});
         return f(Cfg<ST, SM, false, RF, OCC, false, I, FU, P>{});
       };
+      // uniform exits (general-graph native ensembles): same drift kinds
+      auto mku = [&](auto inj_t, auto full_t, auto pp_t) -> cudaError_t {
+        constexpr bool I = decltype(inj_t)::value, FU = decltype(full_t)::value,
+                       P = decltype(pp_t)::value;
+        if constexpr (ENS && !ST && !I) {
+          if (uni) {
+            if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, I, FU, P, false, true>{});
+            if (zd) return f(Cfg<ST, SM, false, RF, OCC, true, I, FU, P, false, true>{});
+            if (cd) return f(Cfg<ST, SM, false, RF, OCC, false, I, FU, P, true, true>{});
+            return f(Cfg<ST, SM, false, RF, OCC, false, I, FU, P, false, true>{});
+          }
+        }
+        return mk(inj_t, full_t, pp_t);
+      };
       if (inj) {  // parity mode: no occupation sampling; state-in, counter, 32-bit counts
         if constexpr (!OCC) return mk(T{}, N{}, T{});
         return cudaErrorInvalidValue;
       }
-      if (full) return mk(N{}, T{}, T{});
+      if (full) return mku(N{}, T{}, T{});
       if constexpr (ENS)
-        if (!pp) return mk(N{}, N{}, N{});  // lean: fused estimators only
-      return mk(N{}, N{}, T{});
+        if (!pp) return mku(N{}, N{}, N{});  // lean: fused estimators only
+      return mku(N{}, N{}, T{});
     };
     if constexpr (ST)
       if (reflect) return drift(T{});
@@ -1502,9 +1540,11 @@ cudaError_t launch_native_ensemble_one(const gsde_graph *g, const gsde_run &a, c
   // per-particle counters only when some per-particle array is requested
   const bool pp = o.edge || o.x || o.crossings || o.events || o.truncs;
   return occ ? dispatch<true, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f, run,
-                                    inj, full, pp, g->const_drift && !generic_drift())
+                                    inj, full, pp, g->const_drift && !generic_drift(),
+                                    g->uniform_exits && !generic_exits())
              : dispatch<false, true>(g->is_star, stage, g->has_tab, g->zero_drift, p.reflect > 0.0f,
-                                     run, inj, full, pp, g->const_drift && !generic_drift());
+                                     run, inj, full, pp, g->const_drift && !generic_drift(),
+                                     g->uniform_exits && !generic_exits());
 }
 
 }  // namespace

@@ -283,3 +283,51 @@ def test_chunked_launches_equal_one_launch(tmp_path):
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
 
+
+_UNI_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2512_02175_b200 as gs
+from paper_2512_02175_b200 import engine, workloads
+out = {{}}
+for name, (g, f) in (("vasc", workloads.vascular(20_000, seed=5)), ("hub64", workloads.hub64())):
+    grid = gs.EdgeGrid.uniform(g, 4)
+    for cap in (100, 3):
+        cfg = gs.SimulationConfig(dt=1e-3, n_steps=200, n_particles=200_001, seed=3,
+                                  initial=gs.PerEdgeUniform(float(g.edge_length.max())),
+                                  max_splits_per_step=cap)
+        for outs in (("edge_counts",), ("all", "edge_counts")):
+            r = engine.ensemble_device(g, f, cfg, outputs=outs, grid=grid, occupation=(5, 2))
+            for k, v in r.items():
+                if not k.startswith("_") and v is not None:
+                    out["%s_c%d_%d_%s" % (name, cap, len(outs), k)] = v.cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_uniform_exit_variant_equals_alias_pick(tmp_path):
+    """Graphs whose every alias column keeps its own slot (equal jump weights at
+    every vertex: C2, C4) pick exits by the column alone; the result must equal
+    the alias pick (GSDE_GENERIC_EXITS=1) bit for bit -- shared-memory and
+    L2-resident tables, lean and per-particle, occupation, a truncating cap."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for generic in (False, True):
+        path = str(tmp_path / f"uni_{int(generic)}.npz")
+        env = dict(os.environ)
+        env.pop("GSDE_GENERIC_EXITS", None)
+        if generic:
+            env["GSDE_GENERIC_EXITS"] = "1"
+        subprocess.run([sys.executable, "-c", _UNI_SCRIPT.format(root=root, path=path)],
+                       check=True, env=env, timeout=600)
+        res[generic] = np.load(path)
+    a, b = res[False], res[True]
+    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 40
+    for k in a.files:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
