@@ -520,7 +520,9 @@ struct Lane {
         events += 1;
         truncs += trunc ? 1 : 0;
       }
-      if (C::HT && trunc) atomicAdd(&S.tot[2], 1ull);  // rare: a step cut at the cap
+      // rare: a step cut at the cap -- a 32-bit shared add on the counter's low
+      // word (a block counts < 2^32 steps; a 64-bit shared atomic is a CAS loop)
+      if (C::HT && trunc) atomicAdd(reinterpret_cast<unsigned *>(&S.tot[2]), 1u);
       mh_add<C::FULL>(S, M > cap ? cap : M);
     }
     M = 0;
@@ -1219,7 +1221,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
       add_i64(&o.exit_counts[L.e], 1);
     mh_add<C::FULL>(S, L.M > p.cap ? p.cap : L.M);
     if constexpr (HT) {
-      if (L.trunc) atomicAdd(&S.tot[2], 1ull);
+      if (L.trunc) atomicAdd(reinterpret_cast<unsigned *>(&S.tot[2]), 1u);
     } else {
       t_M += L.M;
       t_ev += L.M > 0 ? 1 : 0;
