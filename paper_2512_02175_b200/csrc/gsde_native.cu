@@ -264,7 +264,7 @@ struct Cfg {
   // candidate selects, and on L2-resident graphs a 48 B record (the slot and
   // its edge's records) instead of 80 B; the same slot as the alias pick
   static constexpr bool UNI = UNI_;
-  static_assert(!(UNI_ && (STAR_ || INJ_)), "uniform exits: general-graph native kernels");
+  static_assert(!(UNI_ && INJ_), "uniform exits: native-stream kernels");
   static_assert(PP_ || !(INJ_ || FULL_), "INJ / FULL kernels keep per-particle counters");
   using Cnt = std::conditional_t<FULL_, long long, int>;
   static_assert(!(TAB_ && ZD_), "a tabulated drift is not zero");
@@ -590,7 +590,9 @@ __device__ __forceinline__ bool rare_star(Lane<C> &L, const NativeGraph &G,
     L.load_edge(T, O, ref_pick(L, 0, G.n_edges, L.inj_raw()) & 0x7fffffff, p.sqdt, L.len);
     z = L.inj_gauss();
   } else {
-    L.load_edge(T, O, alias_pick(T, 0, G.n_edges, u) & 0x7fffffff, p.sqdt, L.len);
+    const int s = C::UNI ? T.C((int)__umulhi(u, (uint32_t)G.n_edges)).y
+                         : alias_pick(T, 0, G.n_edges, u);
+    L.load_edge(T, O, s & 0x7fffffff, p.sqdt, L.len);
   }
   const float w = fabsf(z);
   const float mu0 = C::TAB ? L.drift(G, 0.0f) : L.mu_a;  // mu(0) = mu_a (+ mu_b * 0)
@@ -1399,7 +1401,9 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
       auto mku = [&](auto inj_t, auto full_t, auto pp_t) -> cudaError_t {
         constexpr bool I = decltype(inj_t)::value, FU = decltype(full_t)::value,
                        P = decltype(pp_t)::value;
-        if constexpr (ENS && !ST && !I) {
+        // (general-graph ensembles; star graphs: the vertex trials, where every
+        // trip is a vertex event)
+        if constexpr (!I && (ENS ? !ST : ST)) {
           if (uni) {
             if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, I, FU, P, false, true>{});
             if (zd) return f(Cfg<ST, SM, false, RF, OCC, true, I, FU, P, false, true>{});
@@ -1638,7 +1642,7 @@ cudaError_t launch_native_trials(const gsde_graph *g, const gsde_trials &a,
     // hand-out from a warp pool kept 40 registers but cost 7%.
     return launch(k, smem, occupancy_grid(k, smem, d, n, kTrialWaves), s, g->nat, p, o, exit_cnt,
                   q);
-  }, inj, full);
+  }, inj, full, true, false, g->uniform_exits && !generic_exits());
 }
 
 cudaError_t launch_histogram(int64_t n, const int64_t *edge, const double *x,

@@ -302,15 +302,23 @@ for name, (g, f) in (("vasc", workloads.vascular(20_000, seed=5)), ("hub64", wor
             for k, v in r.items():
                 if not k.startswith("_") and v is not None:
                     out["%s_c%d_%d_%s" % (name, cap, len(outs), k)] = v.cpu().numpy()
+# star vertex trials (C3's star5: equal jump weights), fused counts and per-trial arrays
+g, f = workloads.star5("linear")
+for per_trial in (False, True):
+    r = engine.trials_device(g, f, 1e-3, 300_001, 7, per_trial=per_trial)
+    for k, v in r.items():
+        if not k.startswith("_") and v is not None:
+            out["trials_%d_%s" % (per_trial, k)] = v.cpu().numpy()
 np.savez({path!r}, **out)
 """
 
 
 def test_uniform_exit_variant_equals_alias_pick(tmp_path):
     """Graphs whose every alias column keeps its own slot (equal jump weights at
-    every vertex: C2, C4) pick exits by the column alone; the result must equal
-    the alias pick (GSDE_GENERIC_EXITS=1) bit for bit -- shared-memory and
-    L2-resident tables, lean and per-particle, occupation, a truncating cap."""
+    every vertex: C2, C4, C3's star) pick exits by the column alone; the result
+    must equal the alias pick (GSDE_GENERIC_EXITS=1) bit for bit -- shared-memory
+    and L2-resident tables, lean and per-particle, occupation, a truncating cap,
+    and the star vertex trials."""
     import os
     import subprocess
     import sys
@@ -327,7 +335,7 @@ def test_uniform_exit_variant_equals_alias_pick(tmp_path):
                        check=True, env=env, timeout=600)
         res[generic] = np.load(path)
     a, b = res[False], res[True]
-    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 40
+    assert sorted(a.files) == sorted(b.files) and len(a.files) >= 46
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
 
