@@ -1,10 +1,8 @@
 mkdir -p gpurun_out/r2b
-timeout 600 python -m pytest tests/test_gpu_distributed.py -q -x > gpurun_out/r2b/dist.txt 2>&1
-echo "rc=$?" >> gpurun_out/r2b/dist.txt
-for w in vascular hub64; do
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:native_ensemble_kernel -c 1 \
-    -o gpurun_out/r2b/ncu_$w python bench.py --workload $w --steps 1 --warmup 0 --no-extras --no-cpu \
-    > gpurun_out/r2b/ncu_$w.log 2>&1
-  echo "$w rc=$?"
-done
+nvidia-smi -L > gpurun_out/r2b/smi.txt
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r2b/pytest_gpu.txt 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2b/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2b/smoke.txt 2>&1
+timeout 900 python bench.py > gpurun_out/r2b/bench.json 2> gpurun_out/r2b/bench.err
+timeout 900 python bench.py --impl reference > gpurun_out/r2b/bench_ref.json 2> gpurun_out/r2b/bench_ref.err
 echo done
