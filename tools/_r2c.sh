@@ -1,5 +1,8 @@
 mkdir -p gpurun_out/r2c
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r2c/pytest_gpu.txt 2>&1
-echo "rc=$?" >> gpurun_out/r2c/pytest_gpu.txt
-A=build_exp/base/libgsde.so B=build_exp/v1/libgsde.so WORKLOADS="star3 hub64 vascular" R=2 N=6 bash tools/ab.sh > gpurun_out/r2c/ab.txt 2>&1
+for t in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $t python tools/sanitize.py > gpurun_out/r2c/san_$t.txt 2>&1
+  echo "$t rc=$?" >> gpurun_out/r2c/san_$t.txt
+done
+GSDE_FORCE_GLOBAL_BINS=1 GSDE_CHUNK_PARTICLES=7777 timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > gpurun_out/r2c/san_memcheck_globalbins_chunked.txt 2>&1
+echo "rc=$?" >> gpurun_out/r2c/san_memcheck_globalbins_chunked.txt
 echo done

@@ -42,6 +42,9 @@ raw = rs.integers(0, 2**63, size=(3000, 210), dtype=np.int64).view(np.uint64)
 inj = (torch.as_tensor(raw.view(np.int64)).cuda(),
        torch.as_tensor(rs.standard_normal((3000, 210))).cuda())
 engine.trials_device(gt, ft, 1e-3, 3000, 3, max_splits=100, inject=inj, precision="native")
+gs5, fs5 = workloads.star5("linear")  # C3's star: uniform-exit vertex trials
+for per_trial in (False, True):
+    engine.trials_device(gs5, fs5, 1e-3, 20000, 5, per_trial=per_trial)
 gp, fp = cases.build("path3", gs)
 gridp = gs.EdgeGrid(counts=np.array([3, 1]), lengths=gp.edge_length)
 fvm.fvm_steps_device(gp, fp, gridp, np.linspace(1, 2, 4), 20, 0.5 * fvm.stability_limit(gp, fp, gridp))
