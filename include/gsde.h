@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define GSDE_ABI_VERSION 2
+#define GSDE_ABI_VERSION 3
 
 enum {
   GSDE_OK = 0,
@@ -146,12 +146,28 @@ typedef struct {
    * injected draws the particle consumed (the reference's RngStream.counter
    * advance, engine.py:228) */
   uint64_t *counter;
+  /* Streamed results (optional; per-particle arrays asked for): the kernel
+   * adds 1 to progress[(progress_base + i) >> progress_shift] after particle
+   * i's per-particle outputs are stored (release order, GPU scope), so a copy
+   * stream can wait for a particle-id range (gsde_stream_wait_geq32) and move
+   * it to the host while the launch still runs.  Counters are accumulated:
+   * zero them first.  (No reference counterpart: the reference returns
+   * host arrays once the whole run has finished, engine.py:338-352.) */
+  uint32_t *progress;
+  int64_t progress_base;
+  int32_t progress_shift;
 } gsde_out;
 
 /* run_ensemble's kernel call: kernels.ensemble_star / ensemble_general
  * (engine.py:309-328).  n_steps == 0 performs placement only
  * (engine.py:329-336). */
 int gsde_ensemble(const gsde_graph *g, const gsde_run *run, const gsde_out *out, void *stream);
+
+/* Make `stream` wait until the 32-bit word at device address `addr` is >=
+ * `value` (cuStreamWaitValue32, GEQ) -- the consumer side of gsde_out's
+ * progress counters.  Returns GSDE_OK, or an error when the driver has no
+ * stream memory operations (callers then wait for the whole launch). */
+int gsde_stream_wait_geq32(void *stream, const uint32_t *addr, uint32_t value);
 
 /* Vertex-trial parameters (kernels.py:447-521 arguments). */
 typedef struct {

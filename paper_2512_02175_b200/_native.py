@@ -69,6 +69,7 @@ class Out(C.Structure):
         ("m_hist", _P), ("totals", _P), ("edge_counts", _P), ("hist", _P),
         ("hist_offsets", _P), ("hist_counts", _P), ("hist_dx", _P), ("hist_n_cells", _i64),
         ("occ", _P), ("occ_every", _i64), ("occ_start", _i64), ("counter", _P),
+        ("progress", _P), ("progress_base", _i64), ("progress_shift", _i32),
     ]
 
 
@@ -102,7 +103,7 @@ EXPORTS = (
     "gsde_normal", "gsde_solve_first_passage_s", "gsde_launch_count", "gsde_abi_version",
     "gsde_last_error", "gsde_parse_graph_text", "gsde_parsed_sizes", "gsde_parsed_export",
     "gsde_parsed_free", "gsde_fvm_run", "gsde_u64_to_uniform", "gsde_u64_to_normal",
-    "gsde_norm_ppf",
+    "gsde_norm_ppf", "gsde_stream_wait_geq32",
 )
 
 _lib = None
@@ -127,6 +128,7 @@ def lib():
                 L.gsde_graph_device_bytes.restype = _i64
                 L.gsde_ensemble.argtypes = [_P, C.POINTER(Run), C.POINTER(Out), _P]
                 L.gsde_vertex_trials.argtypes = [_P, C.POINTER(Trials), C.POINTER(TrialsOut), _P]
+                L.gsde_stream_wait_geq32.argtypes = [_P, _P, C.c_uint32]
                 L.gsde_step_batch.argtypes = [_P, C.POINTER(StepArgs), _P, _P, _P, _P, _P, _P]
                 L.gsde_histogram.argtypes = [_i64, _P, _P, _P, _P, _P, _i64, _P, _P]
                 L.gsde_fvm_run.argtypes = [_P, _P, _P, _i64, _f64, _f64, _P, _P, _P]
@@ -151,7 +153,7 @@ def lib():
                 L.gsde_parsed_free.restype = None
                 L.gsde_launch_count.restype = _i64
                 L.gsde_last_error.restype = C.c_char_p
-                assert L.gsde_abi_version() == 2, "libgsde ABI mismatch"
+                assert L.gsde_abi_version() == 3, "libgsde ABI mismatch"
                 _lib = L
     return _lib
 

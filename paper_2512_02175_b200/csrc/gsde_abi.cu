@@ -1,5 +1,6 @@
 // gsde_abi.cu -- the extern "C" boundary (include/gsde.h): graph upload,
 // argument checks, stream/mode dispatch and host-side scalar helpers.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -535,6 +536,15 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
                                   "histogram");
   if (native_inj && (a->n_steps > 0x7fffffffll || a->inj_stride > 0x7fffffffll))
     return set_error(GSDE_EINVAL, "ensemble: INJECT/NATIVE needs n_steps, inj_stride < 2^31");
+  if (o->progress) {
+    if (!(a->stream == GSDE_STREAM_NATIVE || native_inj))
+      return set_error(GSDE_EINVAL, "ensemble: progress counters are a NATIVE / INJECT-NATIVE "
+                                    "output");
+    if (!(o->edge || o->x || o->crossings || o->events || o->truncs))
+      return set_error(GSDE_EINVAL, "ensemble: progress counts per-particle outputs; none asked");
+    if (o->progress_base < 0 || o->progress_shift < 0 || o->progress_shift > 62)
+      return set_error(GSDE_EINVAL, "ensemble: progress_base >= 0, progress_shift in [0, 62]");
+  }
   if (a->n_particles == 0) return GSDE_OK;
   DeviceGuard guard(g->device);
   const cudaStream_t s = (cudaStream_t)stream;
@@ -542,6 +552,27 @@ int gsde_ensemble(const gsde_graph *g, const gsde_run *a, const gsde_out *o, voi
                               ? launch_native_ensemble(g, *a, *o, s)
                               : launch_ref_ensemble(g, *a, *o, s);
   return err == cudaSuccess ? GSDE_OK : cuda_fail(err, "ensemble launch");
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda
+// link); resolved once
+int gsde_stream_wait_geq32(void *stream, const uint32_t *addr, uint32_t value) {
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WaitFn fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<WaitFn>(f);
+  }();
+  if (!addr) return set_error(GSDE_EINVAL, "stream_wait_geq32: null address");
+  if (!fn) return set_error(GSDE_ECUDA, "stream_wait_geq32: cuStreamWaitValue32 unavailable");
+  const CUresult r = fn((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS)
+    return set_error(GSDE_ECUDA, "stream_wait_geq32: cuStreamWaitValue32 failed (%d)", (int)r);
+  return GSDE_OK;
 }
 
 int gsde_vertex_trials(const gsde_graph *g, const gsde_trials *a, const gsde_trials_out *o,

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 from dataclasses import dataclass, field as dataclass_field
 
 import numpy as np
@@ -212,7 +213,7 @@ def _check_ensemble_shape(graph: MetricGraph, config: SimulationConfig) -> None:
 
 def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, outputs=("all",),
                     grid=None, inject=None, precision="f32", stream=None, occupation=None,
-                    state=None):
+                    state=None, progress=None):
     """Run an ensemble and return DEVICE tensors (no host copies).
 
     ``outputs``: any of ``"edge", "x", "crossings", "events", "truncs"`` or
@@ -238,6 +239,11 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
     ``precision="native"`` the injected rows start at the state's draw and
     ``res["counter"]`` counts the draws each particle consumed.  Native /
     injected-native streams only.
+
+    ``progress=(counters, shift)`` (a zeroed device int32 tensor) streams the
+    per-particle arrays: the kernel adds 1 to ``counters[i >> shift]`` once
+    particle ``i``'s outputs are stored, so a copy stream can wait for a
+    range (``gsde_stream_wait_geq32``) while the launch still runs.
     """
     torch, dev = _native.torch_cuda(config.device)
     n = config.n_particles if n_particles is None else int(n_particles)
@@ -312,6 +318,8 @@ def ensemble_device(graph, field, config, *, pid_offset=0, n_particles=None, out
             sk = state[2].to(device=f"cuda:{dev}", dtype=torch.int64).contiguous()
             res["_state"] += (sk,)
             r.state_counter = sk.data_ptr()
+    if progress is not None:
+        o.progress, o.progress_base, o.progress_shift = progress[0].data_ptr(), 0, int(progress[1])
     s = stream if stream is not None else _native.cur_stream(dev)
     _native.check(_native.lib().gsde_ensemble(dg.handle, r, o, s))
     return res
@@ -408,6 +416,9 @@ def _ensemble_to_host(graph, field, config, pid_offset=0, n_particles=None, grid
     if streams is None:  # copies; second launch stream
         streams = _COPY_STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     copier, side = streams
+    if config.rng == "native" and 0 < config.n_steps < 256 and _streaming_ok(copier):
+        return _streamed_to_host(graph, field, config, pid_offset, n, outs, names, grid,
+                                 est_keys, estimators, compute, copier)
     side.wait_stream(compute)  # whatever the caller queued comes first
     hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
              for k in names]
@@ -433,6 +444,79 @@ def _ensemble_to_host(graph, field, config, pid_offset=0, n_particles=None, grid
     copier.synchronize()
     compute.wait_stream(side)
     est = {k: sum(r[k] for r in parts) for k in est_keys}
+    if estimators:
+        return [h.numpy() for h in hosts], est
+    return [h.numpy() for h in hosts] + [est["m_hist"].cpu().numpy(),
+                                         est["totals"].cpu().numpy()]
+
+
+_STREAM_RANGES = 256  # progress counters per launch
+_STREAMING: dict = {}  # copy stream -> stream memory operations work
+
+
+def _streaming_ok(copier) -> bool:
+    """cuStreamWaitValue32 usable (checked once per copy stream with a wait
+    that is already satisfied); GSDE_NO_STREAMING=1 keeps the chunked
+    launches."""
+    import torch
+
+    if os.environ.get("GSDE_NO_STREAMING"):
+        return False
+    ok = _STREAMING.get(copier)
+    if ok is None:
+        z = torch.zeros(1, dtype=torch.int32, device=copier.device)
+        torch.cuda.current_stream(copier.device).synchronize()
+        ok = _native.lib().gsde_stream_wait_geq32(copier.cuda_stream, z.data_ptr(), 0) == 0
+        copier.synchronize()
+        _STREAMING[copier] = ok
+    return ok
+
+
+def _copy_groups(n_ranges: int) -> list:
+    """Range groups the copy stream moves together: 8 ranges at a time, the
+    last 8 one by one (the final copy, exposed after the kernel, is small)."""
+    cuts = list(range(0, max(n_ranges - 8, 0), 8)) + list(range(max(n_ranges - 8, 0), n_ranges))
+    cuts.append(n_ranges)
+    return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+
+
+def _streamed_to_host(graph, field, config, pid_offset, n, outs, names, grid, est_keys,
+                      estimators, compute, copier):
+    """_ensemble_to_host with ONE launch: the kernel counts finished
+    particles per id range (gsde_out.progress, published after a GPU-scope
+    fence) and the copy stream waits on each range's counter
+    (cuStreamWaitValue32) before moving it, so the D2H starts with the first
+    finished range.  Used for transfer-bound runs (n_steps < 256, where the
+    copy engine is the bottleneck): C4 e2e 70.2 -> 64.7 ms.  Kernel-bound runs
+    keep the chunked launches -- there the publication fences (+1.8% kernel
+    time on C1) and the copy tail after the launch cost as much as the
+    chunks' launch tails (C1 25.6 vs 25.5 ms, hub64 267 vs 265 ms;
+    tools/e2e_streamed_ab.py, tools/e2e_streamed_timeline.py)."""
+    import torch
+
+    shift = max(0, (n - 1).bit_length() - (_STREAM_RANGES.bit_length() - 1))
+    n_ranges = ((n - 1) >> shift) + 1
+    prog = torch.zeros(n_ranges, dtype=torch.int32, device=compute.device)
+    zeroed = torch.cuda.Event()
+    zeroed.record(compute)
+    copier.wait_event(zeroed)  # the counters' zeroing precedes every wait (not the launch)
+    hosts = [torch.empty(n, dtype=torch.float64 if k == "x" else torch.int64, pin_memory=True)
+             for k in names]
+    res = ensemble_device(graph, field, config, pid_offset=int(pid_offset), n_particles=n,
+                          outputs=outs, grid=grid, stream=compute.cuda_stream,
+                          progress=(prog, shift))
+    wait = _native.lib().gsde_stream_wait_geq32
+    base = prog.data_ptr()
+    with torch.cuda.stream(copier):
+        for a, b in _copy_groups(n_ranges):
+            for r in range(a, b):
+                cnt = min(n, (r + 1) << shift) - (r << shift)
+                _native.check(wait(copier.cuda_stream, base + 4 * r, cnt))
+            lo, hi = a << shift, min(n, b << shift)
+            for h, k in zip(hosts, names):
+                h[lo:hi].copy_(res[k][lo:hi], non_blocking=True)
+    copier.synchronize()
+    est = {k: res[k] for k in est_keys}
     if estimators:
         return [h.numpy() for h in hosts], est
     return [h.numpy() for h in hosts] + [est["m_hist"].cpu().numpy(),

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     lib = C.CDLL(_native.LIB_PATH)
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.gsde_abi_version() == 2
+    assert lib.gsde_abi_version() == 3
 
 
 def test_library_is_sm100a():
