@@ -860,19 +860,27 @@ __device__ __forceinline__ void place_native(Lane<C> &L, const NativeGraph &G,
 //  * placements: particle index, edge and position of the next particles,
 //    filled 32 at a time in one converged pass (one atomic, 32 Philox blocks
 //    and 32 edge-record loads in flight together);
-//  * finished states: edge and position awaiting the fused estimators,
-//    binned 32 at a time in one converged pass (the dependent grid loads of
-//    32 particles in flight together).
+//  * finished states: edge and position awaiting the fused estimators --
+//    and, in per-particle kernels, the particle's index and counters
+//    awaiting its output stores -- handled 32 at a time in one converged
+//    pass (the dependent grid loads / stores of 32 particles in flight
+//    together; a store pass per finishing lane ran at ~1 active lane).
 constexpr int kRing = 64;
+template <class Cnt>
 struct WarpQueues {
   long long *pid;
   int *pe;
   float *px;
   int *fe;
   float *fx;
-  int *fr;  // streamed results: progress ranges of finished particles awaiting publication
+  long long *fi;      // per-particle kernels: finished particle index
+  Cnt *fc, *fv, *ft;  //   and its crossings / events / truncations
 };
-constexpr size_t kQueueBytesPerWarp = kRing * (sizeof(long long) + 3 * sizeof(int) + 2 * sizeof(float));
+template <class C>
+__host__ __device__ constexpr size_t queue_bytes_per_warp() {
+  return kRing * (sizeof(long long) + 2 * sizeof(int) + 2 * sizeof(float) +
+                  (C::PP ? sizeof(long long) + 3 * sizeof(typename C::Cnt) : 0));
+}
 
 // Random words of one Q-trip iteration with SLOTS vertex slots (trips
 // k Q / SLOTS): word 0 = slot 0's exit uniform, words 1..Q = Box-Muller
@@ -960,7 +968,6 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
         t_events += L.events;
         t_truncs += L.truncs;
       }
-      epilogue_particle(o, i, L.e, (double)L.x, L.cross, L.events, L.truncs);
     }
     if (C::INJ) t_over += L.over ? 1 : 0;
     if (C::STATE && q.counter)  // next block (NATIVE: carry in id's bits 48..) / draws used (INJ)
@@ -995,15 +1002,21 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
   // their vertex slot.
   const int lane = threadIdx.x & 31;
   extern __shared__ __align__(16) unsigned char smem_q[];
-  WarpQueues WQ;
+  WarpQueues<typename C::Cnt> WQ;
   {
-    unsigned char *q = smem_q + queue_off + (threadIdx.x >> 5) * kQueueBytesPerWarp;
+    unsigned char *q = smem_q + queue_off + (threadIdx.x >> 5) * queue_bytes_per_warp<C>();
     WQ.pid = reinterpret_cast<long long *>(q);
     WQ.pe = reinterpret_cast<int *>(q + kRing * sizeof(long long));
     WQ.px = reinterpret_cast<float *>(q + kRing * (sizeof(long long) + sizeof(int)));
     WQ.fe = reinterpret_cast<int *>(q + kRing * (sizeof(long long) + sizeof(int) + sizeof(float)));
     WQ.fx = reinterpret_cast<float *>(q + kRing * (sizeof(long long) + 2 * sizeof(int) + sizeof(float)));
-    WQ.fr = reinterpret_cast<int *>(q + kRing * (sizeof(long long) + 2 * sizeof(int) + 2 * sizeof(float)));
+    if constexpr (C::PP) {
+      unsigned char *r = q + kRing * (sizeof(long long) + 2 * sizeof(int) + 2 * sizeof(float));
+      WQ.fi = reinterpret_cast<long long *>(r);
+      WQ.fc = reinterpret_cast<typename C::Cnt *>(r + kRing * sizeof(long long));
+      WQ.fv = WQ.fc + kRing;
+      WQ.ft = WQ.fv + kRing;
+    }
   }
   uint32_t q_head = 0, q_tail = 0;  // placement ring (warp-uniform)
   int f_n = 0;                      // finished states queued (warp-uniform)
@@ -1039,62 +1052,62 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
         const unsigned grp = __match_any_sync(0xffffffffu, c);
         if (mine && lane == __ffs(grp) - 1) atomicAdd(&s_h[c], (unsigned)__popc(grp));
       }
-    } else if (mine) {
+    } else if (bins && mine) {
       epilogue_bins(o, WQ.fe[lane], (double)WQ.fx[lane]);
+    }
+    if constexpr (C::PP) {
+      // the per-particle outputs, one particle per lane; then, for streamed
+      // results, one GPU-scope fence for the warp and one relaxed add per
+      // distinct progress range (a release add per particle stalled each
+      // finishing warp on its own fence: +7% kernel time on C1)
+      const long long fi = mine ? WQ.fi[lane] : 0;
+      if (mine)
+        epilogue_particle(o, fi, WQ.fe[lane], (double)WQ.fx[lane], WQ.fc[lane], WQ.fv[lane],
+                          WQ.ft[lane]);
+      if (q.progress) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncwarp();
+        const int r = mine ? (int)((q.progress_base + fi) >> q.progress_shift) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, r);
+        if (mine && lane == __ffs(grp) - 1) atomicAdd(q.progress + r, (unsigned)__popc(grp));
+      }
     }
     __syncwarp();
     if (lane < f_n - n_take) {  // n_take == 32: sources and targets do not overlap
       WQ.fe[lane] = WQ.fe[n_take + lane];
       WQ.fx[lane] = WQ.fx[n_take + lane];
+      if constexpr (C::PP) {
+        WQ.fi[lane] = WQ.fi[n_take + lane];
+        WQ.fc[lane] = WQ.fc[n_take + lane];
+        WQ.fv[lane] = WQ.fv[n_take + lane];
+        WQ.ft[lane] = WQ.ft[n_take + lane];
+      }
     }
     __syncwarp();
     f_n -= n_take;
-  };
-  // Streamed results: finished particles are published 32 at a time -- one
-  // GPU-scope fence for the warp (every lane's per-particle stores), then one
-  // relaxed add per distinct progress range.  (A release add per particle
-  // stalled each finishing warp on its own fence: +7% kernel time on C1.)
-  int p_n = 0;  // finished particles awaiting publication (warp-uniform)
-  auto publish = [&](int n_take) {  // converged: ranges 0..n_take-1
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    __syncwarp();
-    const bool mine = lane < n_take;
-    const int r = mine ? WQ.fr[lane] : -1;
-    const unsigned grp = __match_any_sync(0xffffffffu, r);
-    if (mine && lane == __ffs(grp) - 1) atomicAdd(q.progress + r, (unsigned)__popc(grp));
-    __syncwarp();
-    if (lane < p_n - n_take) WQ.fr[lane] = WQ.fr[n_take + lane];
-    __syncwarp();
-    p_n -= n_take;
   };
   need = true;
   waiting = false;
   for (;;) {
     const unsigned nm = __ballot_sync(0xffffffffu, need);  // finished lanes (+ the start)
     if (nm) {
-      if constexpr (C::PP) {
-        if (q.progress) {  // queue the finished particles' ranges (i: still the old particle)
-          const unsigned pm = __ballot_sync(0xffffffffu, queued);
-          if (queued)
-            WQ.fr[p_n + __popc(pm & ((1u << lane) - 1u))] =
-                (int)((q.progress_base + i) >> q.progress_shift);
-          p_n += __popc(pm);
-          __syncwarp();
-          if (p_n >= 32) publish(32);
-          if (!bins) queued = false;
-        }
-      }
-      if (bins) {  // queue the finished states; bin 32 at a time
+      if (C::PP || bins) {  // queue the finished states (i, L: still the old particle); 32 at a time
         const unsigned qm = __ballot_sync(0xffffffffu, queued);
         if (queued) {
           const int slot = f_n + __popc(qm & ((1u << lane) - 1u));
           WQ.fe[slot] = L.e;
           WQ.fx[slot] = L.x;
+          if constexpr (C::PP) {
+            WQ.fi[slot] = i;
+            WQ.fc[slot] = L.cross;
+            WQ.fv[slot] = L.events;
+            WQ.ft[slot] = L.truncs;
+          }
           queued = false;
         }
         f_n += __popc(qm);
         __syncwarp();
-        if (f_n >= 32) flush_bins(32);
+        if (!C::PP && f_n >= 32) flush_bins(32);
       }
       const int k = __popc(nm);
       if (q_tail - q_head < (uint32_t)k) {  // refill 32 placements
@@ -1147,10 +1160,13 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
       }
       q_head += k;
       __syncwarp();
-      // out of work (idle lanes): publish what is queued now -- the run's
-      // last particles would otherwise wait for the warp's exit
-      if constexpr (C::PP)
-        if (q.progress && p_n > 0 && !__all_sync(0xffffffffu, active)) publish(p_n);
+      // per-particle kernels flush here, after the refill (one call site);
+      // out of work (idle lanes): store / publish what is queued now -- the
+      // run's last particles would otherwise wait for the warp's exit
+      if constexpr (C::PP) {
+        const int t = f_n >= 32 ? 32 : (f_n > 0 && !__all_sync(0xffffffffu, active) ? f_n : 0);
+        if (t > 0) flush_bins(t);
+      }
     }
     if (!__any_sync(0xffffffffu, active)) break;
     uint32_t W[4 * NB];
@@ -1186,8 +1202,7 @@ __global__ void __launch_bounds__(kThreads, C::STAR ? kMinBlocksStar : kMinBlock
     if (C::FULL && blk == 0u) id += 1ull << 48;
     if (active && L.steps_left == 0) finish();
   }
-  if (bins && f_n > 0) flush_bins(f_n);
-  if (C::PP && p_n > 0) publish(p_n);
+  if ((C::PP || bins) && f_n > 0) flush_bins(f_n);
   if (sbins) {
     const unsigned *s_ec = bin_base(), *s_h = s_ec + q.bin_edges;
     __syncthreads();
@@ -1545,7 +1560,7 @@ cudaError_t launch_native_ensemble_one(const gsde_graph *g, const gsde_run &a, c
     // counters carry into the int64 arrays, so no run length overflows them)
     int occ_cells = 0;
     if (C::OCC && o.hist_n_cells <= kOccSmemCells) occ_cells = (int)o.hist_n_cells;
-    const size_t queues = (kThreads / 32) * kQueueBytesPerWarp;
+    const size_t queues = (kThreads / 32) * queue_bytes_per_warp<C>();
     const size_t occ_tab = (C::OCC && g->E <= kOccTabEdges) ? (size_t)g->E * sizeof(float4) : 0;
     size_t smem = align16(smem_bytes(g, a.cap + 1, stage, false, occ_cells)) + queues + occ_tab;
     cudaError_t err = prepare(k, smem);

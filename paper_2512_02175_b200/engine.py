@@ -416,7 +416,8 @@ def _ensemble_to_host(graph, field, config, pid_offset=0, n_particles=None, grid
     if streams is None:  # copies; second launch stream
         streams = _COPY_STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     copier, side = streams
-    if config.rng == "native" and 0 < config.n_steps < 256 and _streaming_ok(copier):
+    if config.rng == "native" and 0 < config.n_steps and (
+            config.n_steps < 256 or os.environ.get("GSDE_FORCE_STREAMING")) and _streaming_ok(copier):
         return _streamed_to_host(graph, field, config, pid_offset, n, outs, names, grid,
                                  est_keys, estimators, compute, copier)
     side.wait_stream(compute)  # whatever the caller queued comes first
