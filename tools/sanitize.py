@@ -42,6 +42,16 @@ raw = rs.integers(0, 2**63, size=(3000, 210), dtype=np.int64).view(np.uint64)
 inj = (torch.as_tensor(raw.view(np.int64)).cuda(),
        torch.as_tensor(rs.standard_normal((3000, 210))).cuda())
 engine.trials_device(gt, ft, 1e-3, 3000, 3, max_splits=100, inject=inj, precision="native")
+# streamed results: per-particle kernels with progress counters (batched
+# stores + publication) and the copy stream waiting on them
+engine._PIPELINE_MIN = 1
+for gg, ff, init in ((*cases.build("star3_bm", gs), gs.AtVertex(0)),
+                     (g, f, gs.PerEdgeUniform(float(g.edge_length.max())))):
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=40, n_particles=30001, seed=4, initial=init)
+    engine._ensemble_to_host(gg, ff, cfg)
+    prog = torch.zeros(64, dtype=torch.int32, device="cuda")
+    engine.ensemble_device(gg, ff, cfg, outputs=("all", "edge_counts"), grid=gs.EdgeGrid.uniform(
+        gg, 4, lengths=None if not gg.is_star else [2.0] * gg.n_edges), progress=(prog, 9))
 gs5, fs5 = workloads.star5("linear")  # C3's star: uniform-exit vertex trials
 for per_trial in (False, True):
     engine.trials_device(gs5, fs5, 1e-3, 20000, 5, per_trial=per_trial)
