@@ -1246,8 +1246,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   // per-lane sums: trials per lane x cap < 2^31 unless the host chose FULL
   typename C::Cnt t_M = 0;
   int32_t t_ev = 0, t_tr = 0, t_over = 0;
+  // the fused estimator (no per-trial arrays, native draws) walks its trials
+  // by stream id alone: one 64-bit add and compare per trial
+  constexpr bool BY_ID = !OUT && !C::INJ;
+  const uint64_t id_end = (uint64_t)(p.id_offset + p.n);
   auto start = [&]() {
-    id = (uint64_t)(p.id_offset + i);
+    if (!BY_ID) id = (uint64_t)(p.id_offset + i);
     // (star: every trial's first trip picks its exit edge, which loads that
     // edge's record, so the start needs none; general: the start edge's
     // endpoint record names the vertex's slots)
@@ -1295,8 +1299,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
       t_ev += L.M > 0 ? 1 : 0;
       t_tr += L.trunc ? 1 : 0;
     }
-    i += stride;
-    active = i < p.n;
+    if constexpr (BY_ID) {
+      id += (uint64_t)stride;
+      active = id < id_end;
+    } else {
+      i += stride;
+      active = i < p.n;
+    }
     if (active) start();
   };
   L.x = 1.0f;
@@ -1304,6 +1313,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksTrials)
   L.ev = make_int4(0, 0, 0, 0);
   L.len = inf;
   L.mu_a = L.mu_b = L.sig = L.sig_sqdt = 0.0f;
+  if (BY_ID) id = (uint64_t)(p.id_offset + i);
   if (active) start();
   // a trial is one macro step started at the vertex: every trip is a vertex
   // trip, so the rare-path step functions run directly
