@@ -489,9 +489,9 @@ def _streamed_to_host(graph, field, config, pid_offset, n, outs, names, grid, es
     (cuStreamWaitValue32) before moving it, so the D2H starts with the first
     finished range.  Used for transfer-bound runs (n_steps < 256, where the
     copy engine is the bottleneck): C4 e2e 70.2 -> 64.7 ms.  Kernel-bound runs
-    keep the chunked launches -- there the publication fences (+1.8% kernel
-    time on C1) and the copy tail after the launch cost as much as the
-    chunks' launch tails (C1 25.6 vs 25.5 ms, hub64 267 vs 265 ms;
+    keep the chunked launches: there the last ranges complete only as the
+    launch ends, and copying them afterwards costs more than the chunks'
+    launch tails (C1 27.0 vs 25.3 ms, hub64 264.0 vs 264.1 ms;
     tools/e2e_streamed_ab.py, tools/e2e_streamed_timeline.py)."""
     import torch
 
