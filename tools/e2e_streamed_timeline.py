@@ -46,3 +46,27 @@ for wname in (sys.argv[1:] or ["star3"]):
              (done <= kend - 0.1).sum(), nr))
     print("   last 12 ranges complete at (ms before the end):", np.round(kend - done[-12:], 3).tolist())
     print("   range completion is monotone except", int((np.diff(done) < -0.05).sum()), "inversions > 50 us")
+    if os.environ.get("TL_ALL"):
+        print("   completion times (ms):", np.round(done, 3).tolist())
+        # the same run's counters read back by the host while the launch runs
+    if os.environ.get("TL_POLL"):
+        torch.cuda.synchronize()
+        prog.zero_()
+        hp = torch.empty(nr, dtype=torch.int32, pin_memory=True)
+        pol = torch.cuda.Stream()
+        t0 = time.perf_counter()
+        r = engine.ensemble_device(g, f, cfg, outputs=names, progress=(prog, shift))
+        k1 = torch.cuda.Event(); k1.record(s)
+        samples = []
+        while not k1.query():
+            with torch.cuda.stream(pol):
+                hp.copy_(prog, non_blocking=True)
+            pol.synchronize()
+            want = np.minimum(n, (np.arange(nr) + 1) << shift) - (np.arange(nr) << shift)
+            samples.append((time.perf_counter() - t0, int((hp.numpy() >= want).sum()),
+                            int(hp.numpy().sum())))
+        tend = time.perf_counter() - t0
+        print("   host polling of the counters (t ms, ranges complete, particles published):")
+        for t, c, p_ in samples[:: max(1, len(samples) // 40)]:
+            print("     %.3f %d %d" % (1e3 * t, c, p_))
+        print("   launch ended by %.3f ms (host)" % (1e3 * tend))
