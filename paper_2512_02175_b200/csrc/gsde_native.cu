@@ -564,6 +564,9 @@ struct Lane {
 // vertex (x == 0, possibly with an unresolved overshoot from an earlier trip)
 // or beyond the optional mirror wall.  Returns true when the macro step
 // completed.
+#ifndef GSDE_STAR_UNI
+#define GSDE_STAR_UNI 0  // uniform-exit pick in star ensembles: measured -0.7% on C1
+#endif
 #ifndef GSDE_STAR_NEG
 #define GSDE_STAR_NEG 0  // measured: star3 -4.7% (the at-vertex flagging costs the region more than the trips save)
 #endif
@@ -1477,9 +1480,9 @@ cudaError_t dispatch(bool star, bool smem, bool tab, bool zd, bool reflect, F &&
       auto mku = [&](auto inj_t, auto full_t, auto pp_t) -> cudaError_t {
         constexpr bool I = decltype(inj_t)::value, FU = decltype(full_t)::value,
                        P = decltype(pp_t)::value;
-        // (general-graph ensembles; star graphs: the vertex trials, where every
-        // trip is a vertex event)
-        if constexpr (!I && (ENS ? !ST : ST)) {
+        // (general-graph ensembles and vertex trials; star ensembles only with
+        // GSDE_STAR_UNI: measured -0.7% on C1, 23.46 -> 23.63 ms)
+        if constexpr (!I && (ENS ? (!ST || GSDE_STAR_UNI) : ST)) {
           if (uni) {
             if (tab) return f(Cfg<ST, SM, true, RF, OCC, false, I, FU, P, false, true>{});
             if (zd) return f(Cfg<ST, SM, false, RF, OCC, true, I, FU, P, false, true>{});
