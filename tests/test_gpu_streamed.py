@@ -145,3 +145,22 @@ def test_kernel_bound_runs_keep_chunked_launches(monkeypatch):
     cfg = gs.SimulationConfig(dt=1e-3, n_steps=300, n_particles=50_000, seed=1,
                               initial=gs.AtVertex(0))
     engine._ensemble_to_host(g, f, cfg)
+
+
+def test_streamed_shard_equals_plain_shard(monkeypatch):
+    """A rank's shard (global-id offset, as parallel.run_ensemble_distributed
+    asks for it) streams like the whole run: progress ranges are launch-relative."""
+    import torch
+
+    monkeypatch.setattr(engine, "_PIPELINE_MIN", 1)
+    g, f = workloads.vascular(20_000, seed=5)
+    cfg = gs.SimulationConfig(dt=1e-3, n_steps=60, n_particles=1_000_000, seed=8,
+                              initial=gs.PerEdgeUniform(float(g.edge_length.max())))
+    off, n = 123_457, 300_001
+    plain = engine.ensemble_device(g, f, cfg, pid_offset=off, n_particles=n, outputs=NAMES)
+    torch.cuda.synchronize()
+    got, est = engine._ensemble_to_host(g, f, cfg, pid_offset=off, n_particles=n,
+                                        estimators=True)
+    for k, b in zip(NAMES, got):
+        np.testing.assert_array_equal(plain[k].cpu().numpy(), b, err_msg=k)
+    np.testing.assert_array_equal(plain["m_hist"].cpu().numpy(), est["m_hist"].cpu().numpy())
