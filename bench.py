@@ -388,7 +388,8 @@ def measured_peaks():
 
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region (NVML in-process,
-    every 50 ms; nvidia-smi subprocesses only if NVML is unavailable)."""
+    initialised before the region and sampled every 10 ms -- C1's timed region is
+    ~0.12 s; nvidia-smi subprocesses every 50 ms only if NVML is unavailable)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -425,8 +426,7 @@ class ClockSampler:
              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
         return [p.strip() for p in out.stdout.strip().split(",")]
 
-    def _run(self):
-        sample = self._nvml() or self._smi
+    def _run(self, sample, every):
         while not self._stop.is_set():
             try:
                 parts = sample()
@@ -434,10 +434,12 @@ class ClockSampler:
                     self.samples.append(parts)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(every)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        nv = self._nvml()
+        sample, every = (nv, 0.01) if nv else (self._smi, 0.05)
+        self._t = threading.Thread(target=self._run, args=(sample, every), daemon=True)
         self._t.start()
         return self
 
