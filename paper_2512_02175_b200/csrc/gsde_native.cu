@@ -564,6 +564,12 @@ struct Lane {
 // vertex (x == 0, possibly with an unresolved overshoot from an earlier trip)
 // or beyond the optional mirror wall.  Returns true when the macro step
 // completed.
+#ifndef GSDE_EARLY_PICK
+#define GSDE_EARLY_PICK 1  // measured: vascular +1.1% (30.03 -> 29.72 ms)
+#endif
+#ifndef GSDE_EARLY_SMEM
+#define GSDE_EARLY_SMEM 0  // shared-memory tables (hub64): +0.06%, spills the tabulated-drift variants
+#endif
 #ifndef GSDE_STAR_UNI
 #define GSDE_STAR_UNI 0  // uniform-exit pick in star ensembles: measured -0.7% on C1
 #endif
@@ -652,6 +658,28 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
   // the vertex, x the vertex
   const bool pend = L.steps_left < 0 && !isnan(L.pz);
   L.steps_left = abs(L.steps_left);
+  // uniform exits on L2-resident graphs (GSDE_EARLY_PICK): the vertex is known
+  // once the overshoot's end is, so the exit record's L2 round trip is issued
+  // before the split-time math and overlaps it (a step that then ends at the
+  // vertex discards it)
+  constexpr bool EARLY = (C::SMEM ? GSDE_EARLY_SMEM : GSDE_EARLY_PICK) && C::UNI && !C::INJ;
+  int4 ec{}, eer{}, eev{};
+  auto early_pick = [&]() {
+    const bool at_v0 = !(L.x > 0.0f);
+    const int off0 = at_v0 ? L.ev.x : L.ev.z, deg0 = at_v0 ? L.ev.y : L.ev.w;
+    if constexpr (C::SMEM) {
+      ec.x = T.C(off0 + (int)__umulhi(u, (uint32_t)deg0)).y;
+      const float4 r = T.E(ec.x & 0x7fffffff);
+      eer = *reinterpret_cast<const int4 *>(&r);
+      eev = T.V(ec.x & 0x7fffffff);
+    } else {
+      const int4 *f = T.ufat + 3 * (off0 + (int)__umulhi(u, (uint32_t)deg0));
+      ec = __ldg(f);
+      eer = __ldg(f + 1);
+      eev = __ldg(f + 2);
+    }
+  };
+  if (EARLY && !pend) early_pick();
   if (pend) {
     L.px = L.x;
     // the proposal that overshot, recomputed bit for bit (a hit on the common
@@ -659,6 +687,7 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
     const float xn =
         fmaf(L.sig * L.sq, L.pz, C::ZD ? L.px : fmaf(L.drift(G, L.px), L.dtr, L.px));
     L.x = xn <= 0.0f ? 0.0f : L.len;
+    if (EARLY) early_pick();
     // (an L1 prefetch of the exit column issued here, ahead of the split
     // math, measured -2.6% on vascular: its address math costs more than the
     // latency it hides at 32 warps / SM)
@@ -685,6 +714,9 @@ __device__ __forceinline__ bool rare_general(Lane<C> &L, const NativeGraph &G,
     s = ref_pick(L, off, deg, L.inj_raw());
     L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
     z = L.inj_gauss();
+  } else if constexpr (EARLY) {  // records loaded above
+    s = ec.x;
+    L.load_edge_rec(O, s & 0x7fffffff, *reinterpret_cast<const float4 *>(&eer), eev, p.sqdt);
   } else if constexpr (C::SMEM && C::UNI) {
     s = T.C(off + (int)__umulhi(u, (uint32_t)deg)).y;
     L.load_edge(T, O, s & 0x7fffffff, p.sqdt, 0.0f);
